@@ -1,0 +1,117 @@
+/*
+ * ws.h — C-ABI of the B200 (sm_100a) warp-specialized GEMM and FlashAttention-forward path.
+ *
+ * This is the drop-in boundary for the reference's hot path. The reference (warpspec, a
+ * header-only C++20 library) has no FFI: its operator API is the `.k` kernel text plus
+ *   - parse_kernel(text) -> KernelGraph           (ref proj/include/warpspec/validate.hpp:349)
+ *   - interpret_sequential(g, Buffers, pid)       (ref proj/include/warpspec/interp.hpp:157)
+ *   - compile_kernel(g, MachineConfig, RunSpec)   (ref proj/include/warpspec/driver.hpp:116)
+ *   - simulate / run_grid                         (ref proj/include/warpspec/sim.hpp:686,
+ *                                                   ref proj/include/warpspec/grid.hpp:140)
+ * The entry points below replace simulate/run_grid for the two kernel shapes the path covers
+ * (SURVEY.md §8a rows a1..a16):
+ *   ws_gemm_tn   <- gemm.k family, c = a . b^T  (ref proj/kernels/gemm.k:2-17,
+ *                   gemm_large.k:3-18, gemm_batched.k:2-22, gemm_act.k:2-18)
+ *   ws_attn_fwd  <- flash-attention .k of SURVEY.md Appendix A (T/C/U coarse pipeline,
+ *                   ref proj/include/warpspec/pipeline.hpp:160-328)
+ * Knobs mirror RunSpec (ref proj/include/warpspec/driver.hpp:42-57): D (aref depth),
+ * P (MMA pipelining depth), persistent, cooperative (2-CTA pair).
+ *
+ * Conventions: plain pointers and sizes only. The caller owns every device buffer; the
+ * library allocates nothing on the device except TMEM and shared memory inside the kernels.
+ * Calls are asynchronous on the given stream and reentrant per stream. No exceptions cross
+ * this boundary: every entry point returns a ws_status; ws_last_error() returns a
+ * thread-local message for the last failing call on this thread.
+ */
+#ifndef WS_H_
+#define WS_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes. 1..12 mirror warpspec::ErrorCode in declaration order
+ * (ref proj/include/warpspec/errors.hpp:10-23) so a host shim can rethrow
+ * CompileError{code} unchanged. */
+typedef enum ws_status {
+  WS_OK = 0,
+  WS_PARSE = 1,
+  WS_TYPE = 2,                 /* bad dtype / argument shape */
+  WS_UNSUPPORTED_KERNEL = 3,   /* kernel shape not covered by this path */
+  WS_PIPELINE_INFEASIBLE = 4,  /* P > D, D < 1, P < 1 (ref pipeline.hpp:84-92) */
+  WS_STAGE_PLAN_AMBIGUOUS = 5,
+  WS_UNLOWERED_AREF = 6,
+  WS_SMEM_OVERFLOW = 7,        /* stage bytes x D over the 227 KB sm_100a limit */
+  WS_INDIVISIBLE_TILE = 8,     /* a dimension is not a multiple of the tile (ref grid.hpp:43-46) */
+  WS_REGISTER_BUDGET = 9,
+  WS_PROTOCOL_VIOLATION = 10,
+  WS_IO = 11,
+  WS_EVAL = 12,
+  WS_CUDA_ERROR = 100          /* a CUDA runtime/driver call failed */
+} ws_status;
+
+/* Element types of the device operands. The reference payloads are `real` (double) or `int`;
+ * on the GPU the storage type is a launch attribute. */
+typedef enum ws_dtype {
+  WS_F32 = 0,
+  WS_F16 = 1,
+  WS_BF16 = 2,
+  WS_E4M3 = 3
+} ws_dtype;
+
+/* c[M x N] (row stride ldc elements) = scale_a*scale_b * a[M x K] . b[N x K]^T
+ * a, b row-major with row strides lda, ldb (elements). fp32 accumulate in TMEM.
+ * in_dtype in {F16, BF16, E4M3}; out_dtype in {F32, BF16, F16}.
+ * Tiling: M % 128 == 0 (M % 256 with cta_pair), N % bn == 0, K % (128 / elem_bytes) == 0. */
+typedef struct ws_gemm_desc {
+  int32_t in_dtype;
+  int32_t out_dtype;
+  int64_t M, N, K;
+  const void* A; int64_t lda;
+  const void* B; int64_t ldb;
+  void* C;       int64_t ldc;
+  float scale_a, scale_b;      /* per-tensor dequant scales (FP8); 1.0 otherwise */
+  int32_t D;                   /* aref depth: smem ring slots; 0 = auto (max that fits) */
+  int32_t P;                   /* MMA k-blocks in flight; 0 = D (commit straight to empty) */
+  int32_t persistent;          /* 1 = one CTA per SM looping over tiles; 0 = one CTA per tile */
+  int32_t cta_pair;            /* 1 = cta_group::2 256-row tiles (cooperative WGs analogue) */
+  int32_t bn;                  /* N tile: 0 = auto, else 128 or 256 */
+  int32_t group_m;             /* raster: tiles grouped by this many M-blocks; 0 = auto */
+} ws_gemm_desc;
+
+/* FlashAttention forward. q,k,v,o: [B, H, S, Dh] contiguous; lse: [B, H, S] fp32 (natural log,
+ * lse = m + log(l)); may be NULL. Only bh in [bh_begin, bh_end) is computed (the multi-GPU
+ * batch*heads shard); bh_end <= 0 means B*H. dtype in {BF16, F16}; Dh in {64, 128};
+ * S % 128 == 0. softmax_scale <= 0 means 1/sqrt(Dh). */
+typedef struct ws_attn_desc {
+  int32_t dtype;
+  int32_t B, H, S, Dh;
+  int32_t causal;
+  float softmax_scale;
+  const void* Q; const void* K; const void* V;
+  void* O;
+  float* LSE;
+  int32_t D;                   /* K/V aref depth; 0 = auto */
+  int32_t bh_begin, bh_end;
+} ws_attn_desc;
+
+ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream);
+ws_status ws_attn_fwd(const ws_attn_desc* desc, void* cuda_stream);
+
+/* Message for the last non-OK status returned on this thread ("" if none). */
+const char* ws_last_error(void);
+
+/* Number of kernel launches this library has issued since load (evidence counter). */
+int64_t ws_launch_count(void);
+
+/* Library version string, e.g. "ws-b200 0.1 sm_100a". */
+const char* ws_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* WS_H_ */

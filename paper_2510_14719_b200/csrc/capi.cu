@@ -1,0 +1,214 @@
+// capi.cu — the C-ABI (include/ws.h): argument validation with the reference's error codes,
+// TMA descriptor construction, kernel selection and launch.
+//
+// Validation mirrors the reference's rejections:
+//   D < 1 / P < 1 / P > D      -> PIPELINE_INFEASIBLE   (ref proj/include/warpspec/driver.hpp:117-118,
+//                                                         ref proj/include/warpspec/pipeline.hpp:84-92)
+//   dimension not tile-aligned -> INDIVISIBLE_TILE      (ref proj/include/warpspec/grid.hpp:43-46)
+//   stage bytes x D too large  -> SMEM_OVERFLOW         (ref proj/include/warpspec/sim.hpp:81-84;
+//                                                         here against the real 227 KB sm_100a limit)
+#include <cuda.h>
+#include <cudaTypedefs.h>
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+
+#include "../../include/ws.h"
+#include "attn_sm100.cuh"
+#include "gemm_sm100.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+std::atomic<int64_t> g_launches{0};
+
+ws_status fail(ws_status s, const std::string& msg) {
+  g_last_error = msg;
+  return s;
+}
+
+#define WS_CUDA_CHECK(expr)                                                                       \
+  do {                                                                                            \
+    cudaError_t e_ = (expr);                                                                      \
+    if (e_ != cudaSuccess)                                                                        \
+      return fail(WS_CUDA_ERROR, std::string(#expr " failed: ") + cudaGetErrorString(e_));        \
+  } while (0)
+
+PFN_cuTensorMapEncodeTiled_v12000 get_encode() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+int elem_bytes(int dt) {
+  switch (dt) {
+    case WS_F32: return 4;
+    case WS_F16: return 2;
+    case WS_BF16: return 2;
+    case WS_E4M3: return 1;
+  }
+  return 0;
+}
+
+CUtensorMapDataType tma_dtype(int dt) {
+  switch (dt) {
+    case WS_F32: return CU_TENSOR_MAP_DATA_TYPE_FLOAT32;
+    case WS_F16: return CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
+    case WS_BF16: return CU_TENSOR_MAP_DATA_TYPE_BFLOAT16;
+    default: return CU_TENSOR_MAP_DATA_TYPE_UINT8;
+  }
+}
+
+// 2-D row-major tensor [rows x cols] with row stride `ld` elements; box [box_rows x box_cols];
+// 128-byte swizzle (box_cols * elem == 128).
+ws_status make_tmap(CUtensorMap* m, const void* ptr, int dt, int64_t rows, int64_t cols, int64_t ld,
+                    uint32_t box_rows, uint32_t box_cols, CUtensorMapL2promotion promo) {
+  auto enc = get_encode();
+  if (!enc) return fail(WS_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  const int eb = elem_bytes(dt);
+  cuuint64_t dims[2] = {static_cast<cuuint64_t>(cols), static_cast<cuuint64_t>(rows)};
+  cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld * eb)};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  if ((reinterpret_cast<uintptr_t>(ptr) & 15) != 0 || (ld * eb) % 16 != 0)
+    return fail(WS_TYPE, "operand base / row stride must be 16-byte aligned for TMA");
+  CUresult r = enc(m, tma_dtype(dt), 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, promo, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(WS_CUDA_ERROR, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
+  return WS_OK;
+}
+
+int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return n;
+}
+
+constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA on sm_100a
+
+template <int IN, int OUT, int BN>
+ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
+  using namespace ws;
+  const int in_dt = d.in_dtype, out_dt = d.out_dtype;
+  const int kbox = 128 / elem_bytes(in_dt);
+  CUtensorMap ta, tb, tc;
+  ws_status s;
+  if ((s = make_tmap(&ta, d.A, in_dt, d.M, d.K, d.lda, GEMM_BM, kbox, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
+    return s;
+  if ((s = make_tmap(&tb, d.B, in_dt, d.N, d.K, d.ldb, BN, kbox, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
+    return s;
+  const int cw = 128 / elem_bytes(out_dt);
+  if ((s = make_tmap(&tc, d.C, out_dt, d.M, d.N, d.ldc, 32, cw, CU_TENSOR_MAP_L2_PROMOTION_NONE)) != WS_OK) return s;
+
+  GemmParams p;
+  p.M = (int)d.M;
+  p.N = (int)d.N;
+  p.K = (int)d.K;
+  p.num_m_blocks = (int)(d.M / GEMM_BM);
+  p.num_n_blocks = (int)(d.N / BN);
+  p.num_k_blocks = (int)(d.K / kbox);
+  const GemmSmemLayout L1 = gemm_smem_layout(BN, 1);
+  int max_stages = (SMEM_LIMIT - (int)(L1.total - L1.stage_bytes)) / (int)L1.stage_bytes;
+  if (max_stages > GEMM_MAX_STAGES) max_stages = GEMM_MAX_STAGES;
+  p.stages = d.D > 0 ? d.D : max_stages;
+  p.mma_depth = d.P > 0 ? d.P : p.stages;
+  if (p.mma_depth > p.stages)
+    return fail(WS_PIPELINE_INFEASIBLE, "MMA pipelining depth P=" + std::to_string(p.mma_depth) +
+                                            " exceeds aref depth D=" + std::to_string(p.stages));
+  const GemmSmemLayout L = gemm_smem_layout(BN, p.stages);
+  if (p.stages > GEMM_MAX_STAGES || (int)L.total > SMEM_LIMIT)
+    return fail(WS_SMEM_OVERFLOW, "D=" + std::to_string(p.stages) + " stages need " + std::to_string(L.total) +
+                                      " B of shared memory; limit " + std::to_string(SMEM_LIMIT));
+  p.group_m = d.group_m > 0 ? d.group_m : 16;
+  if (p.group_m > p.num_m_blocks) p.group_m = p.num_m_blocks;
+  p.scale = d.scale_a * d.scale_b;
+
+  auto kern = ws_gemm_tn_kernel<IN, OUT, BN>;
+  WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+  const int tiles = p.num_m_blocks * p.num_n_blocks;
+  int grid = d.persistent ? (tiles < num_sms() ? tiles : num_sms()) : tiles;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(GEMM_THREADS);
+  cfg.dynamicSmemBytes = L.total;
+  cfg.stream = stream;
+  WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return WS_OK;
+}
+
+template <int IN, int BN>
+ws_status dispatch_out(const ws_gemm_desc& d, cudaStream_t st) {
+  switch (d.out_dtype) {
+    case WS_F32: return launch_gemm<IN, ws::OUT_F32, BN>(d, st);
+    case WS_BF16: return launch_gemm<IN, ws::OUT_BF16, BN>(d, st);
+    case WS_F16: return launch_gemm<IN, ws::OUT_F16, BN>(d, st);
+  }
+  return fail(WS_TYPE, "out_dtype must be F32, BF16 or F16");
+}
+
+template <int BN>
+ws_status dispatch_in(const ws_gemm_desc& d, cudaStream_t st) {
+  switch (d.in_dtype) {
+    case WS_F16: return dispatch_out<ws::IN_F16, BN>(d, st);
+    case WS_BF16: return dispatch_out<ws::IN_BF16, BN>(d, st);
+    case WS_E4M3: return dispatch_out<ws::IN_E4M3, BN>(d, st);
+  }
+  return fail(WS_TYPE, "in_dtype must be F16, BF16 or E4M3");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ws_last_error(void) { return g_last_error.c_str(); }
+int64_t ws_launch_count(void) { return g_launches.load(); }
+const char* ws_version(void) { return "ws-b200 0.1 sm_100a"; }
+
+ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
+  g_last_error.clear();
+  if (!desc) return fail(WS_TYPE, "null descriptor");
+  const ws_gemm_desc& d = *desc;
+  if (d.M <= 0 || d.N <= 0 || d.K <= 0) return fail(WS_TYPE, "M, N, K must be positive");
+  if (!d.A || !d.B || !d.C) return fail(WS_TYPE, "null operand pointer");
+  if (d.D < 0 || d.P < 0) return fail(WS_PIPELINE_INFEASIBLE, "D and P must be >= 1 (0 = auto)");
+  if (d.D > 0 && d.P > d.D)
+    return fail(WS_PIPELINE_INFEASIBLE,
+                "MMA pipelining depth P=" + std::to_string(d.P) + " exceeds aref depth D=" + std::to_string(d.D));
+  const int eb = elem_bytes(d.in_dtype);
+  if (eb == 0 || d.in_dtype == WS_F32) return fail(WS_TYPE, "in_dtype must be F16, BF16 or E4M3");
+  int bn = d.bn > 0 ? d.bn : 256;
+  if (bn != 128 && bn != 256) return fail(WS_TYPE, "bn must be 128 or 256");
+  if (d.cta_pair) return fail(WS_UNSUPPORTED_KERNEL, "cta_pair (cta_group::2) not built in this version");
+  if (d.M % ws::GEMM_BM) return fail(WS_INDIVISIBLE_TILE, "M=" + std::to_string(d.M) + " is not a multiple of 128");
+  if (d.N % bn) return fail(WS_INDIVISIBLE_TILE, "N=" + std::to_string(d.N) + " is not a multiple of bn=" + std::to_string(bn));
+  if (d.K % (128 / eb))
+    return fail(WS_INDIVISIBLE_TILE, "K=" + std::to_string(d.K) + " is not a multiple of " + std::to_string(128 / eb));
+  if (d.lda < d.K || d.ldb < d.K || d.ldc < d.N) return fail(WS_TYPE, "leading dimension smaller than the row");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
+  return bn == 256 ? dispatch_in<256>(d, st) : dispatch_in<128>(d, st);
+}
+
+ws_status ws_attn_fwd(const ws_attn_desc* desc, void* cuda_stream) {
+  g_last_error.clear();
+  if (!desc) return fail(WS_TYPE, "null descriptor");
+  return ws_attn_launch(*desc, reinterpret_cast<cudaStream_t>(cuda_stream), g_last_error, g_launches);
+}
+
+}  // extern "C"

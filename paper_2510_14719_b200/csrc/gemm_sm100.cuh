@@ -1,0 +1,256 @@
+// gemm_sm100.cuh — warp-specialized TN GEMM for sm_100a: c = s * a . b^T
+//
+// Reference semantics: the gemm.k family (ref proj/kernels/gemm.k:2-17): per output tile,
+//   acc = 0; for k in 0..K/BK: acc = dot(a[r, k*BK : +BK], b[cn, k*BK : +BK].T, acc); store c[r, cn]
+// with eval_dot's fp accumulation (ref proj/include/warpspec/tile.hpp:218-247).
+//
+// Warp roles (the reference partitioner's producer WG0 / consumer WG1 split,
+// ref proj/include/warpspec/partition.hpp:227-383, specialised to one warp per role):
+//   warp 0      TMA producer: put(a_tile, b_tile) into the smem aref (depth D)
+//   warp 1      MMA issuer: get -> BK/UMMA_K tcgen05.mma into a TMEM accumulator -> consumed
+//               by tcgen05.commit; the accumulator is itself a depth-2 aref (TMEM full/empty)
+//   warp 2      TMEM allocator
+//   warps 4..7  epilogue: tcgen05.ld -> scale/convert -> swizzled smem -> TMA store
+// Persistent scheduling (ref proj/include/warpspec/grid.hpp:93-123, run_grid :140-210): tile t
+// runs on CTA t mod gridDim.x; no per-tile barrier reset or quiesce — the aref phases carry over.
+#pragma once
+
+#include "ws_aref.cuh"
+
+namespace ws {
+
+constexpr int GEMM_BM = 128;           // rows per CTA tile (one TMEM lane per row)
+constexpr int GEMM_ROW_BYTES = 128;    // one 128-byte swizzle row of K per stage
+constexpr int GEMM_MAX_STAGES = 8;
+constexpr int GEMM_THREADS = 256;      // 8 warps
+constexpr int GEMM_EPI_WARP0 = 4;
+constexpr int GEMM_EPI_BUF_BYTES = 32 * 128;  // per epilogue warp per buffer: 32 rows x 128 B
+
+enum InFmt : int { IN_F16 = 0, IN_BF16 = 1, IN_E4M3 = 2 };
+enum OutFmt : int { OUT_F32 = 0, OUT_BF16 = 1, OUT_F16 = 2 };
+
+struct GemmParams {
+  int M, N, K;
+  int num_m_blocks, num_n_blocks, num_k_blocks;
+  int stages;     // D
+  int mma_depth;  // P
+  int group_m;
+  float scale;
+};
+
+struct GemmSmemLayout {
+  uint32_t a_bytes, b_bytes, stage_bytes, epi_offset, bar_offset, total;
+};
+
+__host__ __device__ inline GemmSmemLayout gemm_smem_layout(int bn, int stages) {
+  GemmSmemLayout L;
+  L.a_bytes = GEMM_BM * GEMM_ROW_BYTES;
+  L.b_bytes = bn * GEMM_ROW_BYTES;
+  L.stage_bytes = L.a_bytes + L.b_bytes;
+  L.epi_offset = stages * L.stage_bytes;
+  L.bar_offset = L.epi_offset + 4 * 2 * GEMM_EPI_BUF_BYTES;
+  // full[MAX], empty[MAX], tmem_full[2], tmem_empty[2], tmem base word
+  L.total = L.bar_offset + (2 * GEMM_MAX_STAGES + 4) * 8 + 16 + 1024 /* alignment slack */;
+  return L;
+}
+
+// Tile order: grouped raster over (m, n) blocks so that a wave of CTAs shares A and B panels in
+// L2. The set of tiles equals the .k pid set {pm + pn * TM}; only the visiting order changes.
+__device__ __forceinline__ void gemm_tile_coords(int t, const GemmParams& p, int& mb, int& nb) {
+  int per_group = p.group_m * p.num_n_blocks;
+  int g = t / per_group;
+  int first_m = g * p.group_m;
+  int gsize = min(p.num_m_blocks - first_m, p.group_m);
+  int r = t - g * per_group;
+  mb = first_m + r % gsize;
+  nb = r / gsize;
+}
+
+template <int IN, int OUT, int BN>
+__global__ void __launch_bounds__(GEMM_THREADS, 1)
+    ws_gemm_tn_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
+                      const __grid_constant__ CUtensorMap tm_c, const GemmParams p) {
+  constexpr uint32_t TMEM_COLS = 2 * BN <= 256 ? 256 : 512;  // two accumulator buffers
+  constexpr int OUT_BYTES = OUT == OUT_F32 ? 4 : 2;
+  constexpr int CW = 128 / OUT_BYTES;  // epilogue chunk: output columns per 128-byte row
+  constexpr int UMMA_K_BYTES = 32;     // 16 x 16-bit or 32 x 8-bit per tcgen05.mma
+  constexpr int KSTEPS = GEMM_ROW_BYTES / UMMA_K_BYTES;
+  constexpr uint32_t IDESC = make_idesc(IN == IN_BF16 ? 1u : 0u, GEMM_BM, BN, 0, 0);
+
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const GemmSmemLayout L = gemm_smem_layout(BN, p.stages);
+  auto* ring = reinterpret_cast<ArefBarriers<GEMM_MAX_STAGES>*>(smem + L.bar_offset);
+  uint64_t* tmem_full = reinterpret_cast<uint64_t*>(smem + L.bar_offset + 2 * GEMM_MAX_STAGES * 8);
+  uint64_t* tmem_empty = tmem_full + 2;
+  uint32_t* tmem_base_slot = reinterpret_cast<uint32_t*>(tmem_empty + 2);
+
+  const uint32_t warp = warp_id();
+  const uint32_t lane = lane_id();
+  const int num_tiles = p.num_m_blocks * p.num_n_blocks;
+  const uint32_t D = static_cast<uint32_t>(p.stages);
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch_desc(&tm_a);
+    tma_prefetch_desc(&tm_b);
+    tma_prefetch_desc(&tm_c);
+    ring->init(D, 1, 1);
+    for (int i = 0; i < 2; ++i) {
+      mbar_init(&tmem_full[i], 1);
+      mbar_init(&tmem_empty[i], 4);  // one arrival per epilogue warp
+    }
+    fence_barrier_init();
+  } else if (warp == 2) {
+    tmem_alloc<1>(tmem_base_slot, TMEM_COLS);
+    tmem_relinquish<1>();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem_base = *tmem_base_slot;
+
+  if (warp == 0) {
+    // ===================== TMA producer: aref put =====================
+    if (lane == 0) {
+      ArefCursor c;
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        int mb, nb;
+        gemm_tile_coords(t, p, mb, nb);
+        for (int kb = 0; kb < p.num_k_blocks; ++kb) {
+          ring->put_acquire(c, 1);
+          ring->put_expect(c, L.stage_bytes);
+          uint8_t* sa = smem + c.slot * L.stage_bytes;
+          uint8_t* sb = sa + L.a_bytes;
+          // coordinates are in elements of the tensor map's innermost dim (K) then rows
+          const int kcoord = kb * (IN == IN_E4M3 ? 128 : 64);
+          tma_load_2d(sa, &tm_a, &ring->full[c.slot], kcoord, mb * GEMM_BM);
+          tma_load_2d(sb, &tm_b, &ring->full[c.slot], kcoord, nb * BN);
+          c.advance(D);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ===================== MMA issuer: aref get / consumed =====================
+    if (lane == 0) {
+      ArefCursor c;
+      uint32_t gk = 0;  // global k-block counter (for the literal P window)
+      uint32_t acc_stage = 0, acc_phase = 0;
+      const uint32_t P = static_cast<uint32_t>(p.mma_depth);
+      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+        mbar_wait(&tmem_empty[acc_stage], acc_phase ^ 1u, 3);
+        tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc_stage * BN;
+        for (int kb = 0; kb < p.num_k_blocks; ++kb, ++gk) {
+          if (P < D && gk >= P) {
+            // at most P k-blocks of MMAs in flight (ref pipeline.hpp:98-140, "wait <= P-1")
+            const uint32_t old = gk - P;
+            mbar_wait(&ring->empty[old % D], (old / D) & 1u, 4);
+          }
+          ring->get(c, 2);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + c.slot * L.stage_bytes);
+          const uint32_t sb = sa + L.a_bytes;
+#pragma unroll
+          for (int k = 0; k < KSTEPS; ++k) {
+            const uint64_t ad = make_sw128_desc(sa + k * UMMA_K_BYTES, 16, 1024);
+            const uint64_t bd = make_sw128_desc(sb + k * UMMA_K_BYTES, 16, 1024);
+            if constexpr (IN == IN_E4M3)
+              mma_f8_ss<1>(d_tmem, ad, bd, IDESC, (kb | k) != 0);
+            else
+              mma_f16_ss<1>(d_tmem, ad, bd, IDESC, (kb | k) != 0);
+          }
+          ring->consumed_by_mma(c);
+          c.advance(D);
+        }
+        mma_commit(&tmem_full[acc_stage]);  // accumulator aref: put by the tensor core
+        if (++acc_stage == 2) {
+          acc_stage = 0;
+          acc_phase ^= 1u;
+        }
+      }
+    }
+  } else if (warp >= GEMM_EPI_WARP0) {
+    // ===================== epilogue: TMEM -> regs -> smem -> TMA store =====================
+    const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
+    uint8_t* stage_base = smem + L.epi_offset + q * 2 * GEMM_EPI_BUF_BYTES;
+    uint32_t acc_stage = 0, acc_phase = 0, chunk_ctr = 0;
+    const float scale = p.scale;
+    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      int mb, nb;
+      gemm_tile_coords(t, p, mb, nb);
+      mbar_wait(&tmem_full[acc_stage], acc_phase, 5);
+      tc_fence_after();
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc_stage * BN;
+#pragma unroll 1
+      for (int ch = 0; ch < BN / CW; ++ch, ++chunk_ctr) {
+        uint32_t v[CW];
+        if constexpr (CW == 64) {
+          tmem_ld32(t_row + ch * CW, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+          tmem_ld32(t_row + ch * CW + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+        } else {
+          tmem_ld32(t_row + ch * CW, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+        }
+        tmem_wait_ld();
+        if (ch == BN / CW - 1) {
+          // accumulator fully read: release it to the MMA warp (accumulator aref consumed)
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tmem_empty[acc_stage]);
+        }
+        uint8_t* buf = stage_base + (chunk_ctr & 1u) * GEMM_EPI_BUF_BYTES;
+        if (chunk_ctr >= 2) {
+          if (lane == 0) tma_store_wait_read<1>();  // the store that last used this buffer has read it
+          __syncwarp();
+        }
+        // row `lane` of this warp's 32-row slab: 8 x 16-byte chunks, 128B-swizzled
+        const uint32_t row_addr = smem_u32(buf) + lane * 128u;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          uint32_t w0, w1, w2, w3;
+          if constexpr (OUT == OUT_F32) {
+            w0 = __float_as_uint(__uint_as_float(v[4 * j + 0]) * scale);
+            w1 = __float_as_uint(__uint_as_float(v[4 * j + 1]) * scale);
+            w2 = __float_as_uint(__uint_as_float(v[4 * j + 2]) * scale);
+            w3 = __float_as_uint(__uint_as_float(v[4 * j + 3]) * scale);
+          } else {
+            float f[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[8 * j + e]) * scale;
+            if constexpr (OUT == OUT_BF16) {
+              w0 = pack_bf16(f[0], f[1]);
+              w1 = pack_bf16(f[2], f[3]);
+              w2 = pack_bf16(f[4], f[5]);
+              w3 = pack_bf16(f[6], f[7]);
+            } else {
+              w0 = pack_f16(f[0], f[1]);
+              w1 = pack_f16(f[2], f[3]);
+              w2 = pack_f16(f[4], f[5]);
+              w3 = pack_f16(f[6], f[7]);
+            }
+          }
+          st_shared_v4(row_addr + ((j ^ (lane & 7u)) << 4), w0, w1, w2, w3);
+        }
+        fence_proxy_async_smem();
+        __syncwarp();
+        if (lane == 0) {
+          tma_store_2d(&tm_c, buf, nb * BN + ch * CW, mb * GEMM_BM + q * 32);
+          tma_store_commit();
+        }
+      }
+      if (++acc_stage == 2) {
+        acc_stage = 0;
+        acc_phase ^= 1u;
+      }
+    }
+    if (lane == 0) tma_store_wait<0>();
+  }
+
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc<1>(tmem_base, TMEM_COLS);
+  }
+}
+
+}  // namespace ws

@@ -1,0 +1,106 @@
+"""Host-side mirror of the reference operator interface for the hot path.
+
+The reference runs a `.k` kernel per pid with `interpret_sequential(g, buffers, ExecContext{pid})`
+(ref proj/include/warpspec/interp.hpp:157-185) or through `simulate` / `run_grid`
+(ref proj/include/warpspec/sim.hpp:686, grid.hpp:140). On B200 the two kernel shapes of the path
+run as one launch each over all pids:
+
+  gemm_tn(a, b)        <- gemm.k family: c = a . b^T  (ref proj/kernels/gemm.k:2-17)
+  attn_fwd(q, k, v)    <- the flash .k of SURVEY.md Appendix A (o = acc / l, lse = m + log l)
+
+Both call the C-ABI (include/ws.h) through ctypes on torch's current CUDA stream. Torch is only
+used for device memory and streams. Knob names follow RunSpec (ref driver.hpp:42-57).
+"""
+from __future__ import annotations
+
+import ctypes
+import math
+from typing import Optional
+
+import torch
+
+from . import _lib
+
+_DT = {torch.float32: _lib.WS_F32, torch.float16: _lib.WS_F16, torch.bfloat16: _lib.WS_BF16,
+       torch.float8_e4m3fn: _lib.WS_E4M3}
+
+
+def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return s.cuda_stream
+
+
+def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None, *,
+            out_dtype: Optional[torch.dtype] = None, scale_a: float = 1.0, scale_b: float = 1.0,
+            D: int = 0, P: int = 0, persistent: bool = True, cta_pair: bool = False, bn: int = 0,
+            group_m: int = 0, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
+    """c[M,N] = scale_a*scale_b * a[M,K] . b[N,K]^T with fp32 accumulation on the tensor cores.
+
+    a, b: row-major (last dim contiguous) CUDA tensors of dtype f16/bf16/float8_e4m3fn.
+    out: optional [M,N] tensor (may be a column slice of a wider matrix; its row stride is ldc).
+    """
+    if a.device.type != "cuda" or b.device.type != "cuda":
+        raise _lib.WsError(2, "operands must be CUDA tensors (no CPU path)")
+    if a.dtype != b.dtype or a.dtype not in (torch.float16, torch.bfloat16, torch.float8_e4m3fn):
+        raise _lib.WsError(2, f"unsupported operand dtypes {a.dtype}, {b.dtype}")
+    M, K = a.shape
+    N, K2 = b.shape
+    if K != K2:
+        raise _lib.WsError(2, f"inner dimensions disagree: {K} vs {K2}")
+    if a.stride(1) != 1 or b.stride(1) != 1:
+        raise _lib.WsError(2, "operands must be K-contiguous (row-major)")
+    if out is None:
+        od = out_dtype or (torch.bfloat16 if a.dtype == torch.float8_e4m3fn else a.dtype)
+        out = torch.empty((M, N), dtype=od, device=a.device)
+    if out.stride(1) != 1 or tuple(out.shape) != (M, N):
+        raise _lib.WsError(2, "out must be [M, N] with contiguous rows")
+    d = _lib.GemmDesc()
+    d.in_dtype = _DT[a.dtype]
+    d.out_dtype = _DT[out.dtype]
+    d.M, d.N, d.K = M, N, K
+    d.A, d.lda = a.data_ptr(), a.stride(0)
+    d.B, d.ldb = b.data_ptr(), b.stride(0)
+    d.C, d.ldc = out.data_ptr(), out.stride(0)
+    d.scale_a, d.scale_b = scale_a, scale_b
+    d.D, d.P = D, P
+    d.persistent, d.cta_pair, d.bn, d.group_m = int(persistent), int(cta_pair), bn, group_m
+    lib = _lib.load()
+    _lib.check(lib.ws_gemm_tn(ctypes.byref(d), ctypes.c_void_p(_stream_ptr(stream))))
+    return out
+
+
+def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool = False,
+             softmax_scale: Optional[float] = None, out: Optional[torch.Tensor] = None,
+             lse: Optional[torch.Tensor] = None, D: int = 0, bh_range: Optional[tuple] = None,
+             stream: Optional[torch.cuda.Stream] = None):
+    """FlashAttention forward over [B, H, S, Dh] tensors. Returns (o, lse) with lse fp32 [B, H, S]
+    in natural-log units (lse = m + log l of the .k's running max m and row sum l)."""
+    if q.device.type != "cuda":
+        raise _lib.WsError(2, "operands must be CUDA tensors (no CPU path)")
+    if not (q.dtype == k.dtype == v.dtype) or q.dtype not in (torch.float16, torch.bfloat16):
+        raise _lib.WsError(2, f"unsupported dtype {q.dtype}")
+    B, H, S, Dh = q.shape
+    for t in (q, k, v):
+        if tuple(t.shape) != (B, H, S, Dh) or not t.is_contiguous():
+            raise _lib.WsError(2, "q, k, v must be contiguous [B, H, S, Dh]")
+    if out is None:
+        out = torch.empty_like(q)
+    if lse is None:
+        lse = torch.empty((B, H, S), dtype=torch.float32, device=q.device)
+    d = _lib.AttnDesc()
+    d.dtype = _DT[q.dtype]
+    d.B, d.H, d.S, d.Dh = B, H, S, Dh
+    d.causal = int(causal)
+    d.softmax_scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(Dh)
+    d.Q, d.K, d.V, d.O = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr()
+    d.LSE = lse.data_ptr()
+    d.D = D
+    lo, hi = bh_range if bh_range is not None else (0, B * H)
+    d.bh_begin, d.bh_end = lo, hi
+    lib = _lib.load()
+    _lib.check(lib.ws_attn_fwd(ctypes.byref(d), ctypes.c_void_p(_stream_ptr(stream))))
+    return out, lse
+
+
+def launch_count() -> int:
+    return int(_lib.load().ws_launch_count())
