@@ -1,0 +1,130 @@
+"""`.k` kernel instances for the hot path, in the reference grammar (ref SPEC.md:120-134,
+ref proj/include/warpspec/parse.hpp:412-686). TEST INFRASTRUCTURE: these are the checker's
+inputs, the analogue of the reference fixtures (ref proj/tests/support/fixtures.hpp:14-145).
+
+gemm_src      — real-valued gemm.k (ref proj/kernels/gemm.k:2-17): c = a . b^T, pid column-major
+                over TM x TN output tiles (pm = pid mod TM, pn = pid div TM).
+gemm_int_src  — the shipped integer form (same shape as the reference fixture gemm_tiled_src).
+flash_src     — FlashAttention forward of SURVEY.md Appendix A (batched over B*H slices, causal via
+                the mask bank `mb`), emitting acc, row sum l and running max m.
+"""
+from __future__ import annotations
+
+import math
+
+
+def gemm_src(M: int, N: int, K: int, BM: int, BN: int, BK: int, elem: str = "real",
+             scale: float | None = None) -> str:
+    assert M % BM == 0 and N % BN == 0 and K % BK == 0
+    tm = M // BM
+    lines = [
+        f"kernel gemm(a: buf<{M}x{K} {elem}>, b: buf<{N}x{K} {elem}>, c: buf<{M}x{N} {elem}>) {{",
+        "  %p = pid",
+        f"  %pm = mod %p, {tm}",
+        f"  %pn = div %p, {tm}",
+        f"  %r = mul %pm, {BM}",
+        f"  %cn = mul %pn, {BN}",
+        f"  %z = const zeros : {BM}x{BN} {elem}",
+        "  %k0 = const 0",
+    ]
+    if scale is not None:
+        lines.append(f"  %s = const [[{scale!r}]] : 1x1 {elem}")
+    lines += [
+        f"  loop %k in 0..{K // BK} iter (%acc = %z, %ok = %k0) {{",
+        f"    %ta = tma_load a[%r, %ok] : {BM}x{BK} {elem}",
+        f"    %tb = tma_load b[%cn, %ok] : {BN}x{BK} {elem}",
+        "    %acc1 = dot %ta, %tb.T, acc=%acc",
+        f"    %ok1 = add %ok, {BK}",
+        "    yield %acc1, %ok1",
+        "  }",
+    ]
+    if scale is not None:
+        lines += ["  %o = ew mul %acc, %s", "  store c[%r, %cn] = %o"]
+    else:
+        lines.append("  store c[%r, %cn] = %acc")
+    lines.append("}")
+    return "\n".join(lines) + "\n"
+
+
+def gemm_tiles(M: int, N: int, BM: int, BN: int) -> int:
+    return (M // BM) * (N // BN)
+
+
+def flash_src(BH: int, S: int, D: int, BR: int, causal: bool, scale: float | None = None) -> str:
+    """Batched flash .k over (B*H*S) x D rows; pid = bh * (S/BR) + query block (BR == BC)."""
+    BC = BR
+    nqb = S // BR
+    rows = BH * S
+    sc = scale if scale is not None else 1.0 / math.sqrt(D)
+    L = [
+        f"kernel flash(q: buf<{rows}x{D} real>, k: buf<{rows}x{D} real>, v: buf<{rows}x{D} real>, "
+        f"mb: buf<{BR}x{3 * BC} real>, o: buf<{rows}x{D} real>, lsum: buf<{rows}x1 real>, "
+        f"mx: buf<{rows}x1 real>) {{",
+        "  %p = pid",
+        f"  %bh = div %p, {nqb}",
+        f"  %qb = mod %p, {nqb}",
+        f"  %r = mul %p, {BR}",
+        f"  %kvb = mul %bh, {S}",
+        f"  %zacc = const zeros : {BR}x{D} real",
+        f"  %zc = const zeros : {BR}x1 real",
+        "  %ninf = const [[-1000000.0]] : 1x1 real",
+        "  %m0 = ew add %zc, %ninf",
+        f"  %sc = const [[{sc!r}]] : 1x1 real",
+        "  %k0 = const 0",
+    ]
+    if not causal:
+        L.append(f"  %zs = const zeros : {BR}x{BC} real")
+    L.append(f"  loop %j in 0..{S // BC} iter (%acc = %zacc, %m = %m0, %l = %zc, %ok = %kvb) {{")
+    L.append(f"    %tq = tma_load q[%r, 0] : {BR}x{D} real")
+    L.append(f"    %tk = tma_load k[%ok, 0] : {BC}x{D} real")
+    if causal:
+        # sel = x/NB + (x-1)/NB with x = j - qb + NB: 0 below, 1 on, 2 above the diagonal
+        L += [
+            "    %x0 = sub %j, %qb",
+            f"    %x = add %x0, {nqb}",
+            f"    %s0 = div %x, {nqb}",
+            "    %xm = sub %x, 1",
+            f"    %s1 = div %xm, {nqb}",
+            "    %sel = add %s0, %s1",
+            f"    %mc = mul %sel, {BC}",
+            f"    %tm = tma_load mb[0, %mc] : {BR}x{BC} real",
+            "    %s = dot %tq, %tk.T, acc=%tm",
+        ]
+    else:
+        L.append("    %s = dot %tq, %tk.T, acc=%zs")
+    L += [
+        f"    %tv = tma_load v[%ok, 0] : {BC}x{D} real",
+        "    %ss = ew mul %s, %sc",
+        "    %rm = reduce max %ss axis=1",
+        "    %mn = ew max %m, %rm",
+        "    %d = ew sub %ss, %mn",
+        "    %pp = ew exp %d",
+        "    %dm = ew sub %m, %mn",
+        "    %al = ew exp %dm",
+        "    %rs = reduce add %pp axis=1",
+        "    %la = ew mul %l, %al",
+        "    %l1 = ew add %la, %rs",
+        "    %as = ew mul %acc, %al",
+        "    %acc1 = dot %pp, %tv, acc=%as",
+        f"    %ok1 = add %ok, {BC}",
+        "    yield %acc1, %mn, %l1, %ok1",
+        "  }",
+        "  store o[%r, 0] = %acc",
+        "  store lsum[%r, 0] = %l",
+        "  store mx[%r, 0] = %m",
+        "}",
+    ]
+    return "\n".join(L) + "\n"
+
+
+def flash_mask_bank(BR: int):
+    """The causal mask bank [0 | lower-tri(0)/upper(-1e7) | -1e7]."""
+    import numpy as np
+    BC = BR
+    mb = np.zeros((BR, 3 * BC))
+    for r in range(BR):
+        for c in range(BC):
+            if c > r:
+                mb[r, BC + c] = -1e7
+    mb[:, 2 * BC:] = -1e7
+    return mb

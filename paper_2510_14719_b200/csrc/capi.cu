@@ -173,6 +173,66 @@ ws_status dispatch_in(const ws_gemm_desc& d, cudaStream_t st) {
   return fail(WS_TYPE, "in_dtype must be F16, BF16 or E4M3");
 }
 
+
+template <int DH, bool BF16>
+ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stream) {
+  using namespace ws;
+  const int dt = d.dtype;
+  const int64_t rows = (int64_t)d.B * d.H * d.S;
+  CUtensorMap tq, tk, tv;
+  ws_status s;
+  if ((s = make_tmap(&tq, d.Q, dt, rows, DH, DH, ATTN_BM, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
+  if ((s = make_tmap(&tk, d.K, dt, rows, DH, DH, ATTN_BN, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
+  if ((s = make_tmap(&tv, d.V, dt, rows, DH, DH, ATTN_BN, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
+  AttnParams p;
+  p.S = d.S;
+  p.Dh = DH;
+  p.BH_begin = bh0;
+  p.num_pairs = d.S / (2 * ATTN_BM);
+  p.causal = d.causal;
+  const float sm = d.softmax_scale > 0.f ? d.softmax_scale : 1.0f / std::sqrt((float)DH);
+  p.scale_log2 = sm * 1.4426950408889634f;
+  p.lse = d.LSE;
+  p.o = d.O;
+  p.o_elem = BF16 ? 0 : 1;
+  int max_stages = (SMEM_LIMIT - (int)attn_smem_bytes(DH, 0)) / (int)attn_tile_bytes(DH);
+  if (max_stages > ATTN_MAX_KV_STAGES) max_stages = ATTN_MAX_KV_STAGES;
+  p.kv_stages = d.D > 0 ? d.D : max_stages;
+  if (p.kv_stages < 2)
+    return fail(WS_PIPELINE_INFEASIBLE, "the K/V aref needs D >= 2 (ref pipeline.hpp:309-315)");
+  const uint32_t smem = attn_smem_bytes(DH, p.kv_stages);
+  if (p.kv_stages > ATTN_MAX_KV_STAGES || (int)smem > SMEM_LIMIT)
+    return fail(WS_SMEM_OVERFLOW, "D=" + std::to_string(p.kv_stages) + " K/V stages need " + std::to_string(smem) +
+                                      " B of shared memory; limit " + std::to_string(SMEM_LIMIT));
+  auto kern = ws_attn_fwd_kernel<DH, BF16>;
+  WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(bh1 - bh0, p.num_pairs);
+  cfg.blockDim = dim3(ATTN_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, p));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return WS_OK;
+}
+
+ws_status attn_entry(const ws_attn_desc& d, cudaStream_t st) {
+  if (d.dtype != WS_BF16 && d.dtype != WS_F16) return fail(WS_TYPE, "attention dtype must be BF16 or F16");
+  if (d.B <= 0 || d.H <= 0 || d.S <= 0) return fail(WS_TYPE, "B, H, S must be positive");
+  if (d.Dh != 64 && d.Dh != 128) return fail(WS_UNSUPPORTED_KERNEL, "head dim must be 64 or 128");
+  if (d.S % 256) return fail(WS_INDIVISIBLE_TILE, "S=" + std::to_string(d.S) + " is not a multiple of 256");
+  if (!d.Q || !d.K || !d.V || !d.O) return fail(WS_TYPE, "null operand pointer");
+  if (d.D == 1) return fail(WS_PIPELINE_INFEASIBLE, "the K/V aref needs D >= 2 (ref pipeline.hpp:309-315)");
+  if (d.D < 0) return fail(WS_PIPELINE_INFEASIBLE, "D must be >= 2 (0 = auto)");
+  const int BH = d.B * d.H;
+  const int bh0 = d.bh_begin, bh1 = d.bh_end > 0 ? d.bh_end : BH;
+  if (bh0 < 0 || bh1 > BH || bh0 >= bh1) return fail(WS_TYPE, "bad (b,h) shard range");
+  if ((int64_t)BH * d.S >= (int64_t)1 << 31) return fail(WS_TYPE, "B*H*S must fit in int32");
+  if (d.Dh == 128)
+    return d.dtype == WS_BF16 ? launch_attn<128, true>(d, bh0, bh1, st) : launch_attn<128, false>(d, bh0, bh1, st);
+  return d.dtype == WS_BF16 ? launch_attn<64, true>(d, bh0, bh1, st) : launch_attn<64, false>(d, bh0, bh1, st);
+}
+
 }  // namespace
 
 extern "C" {
@@ -208,7 +268,7 @@ ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
 ws_status ws_attn_fwd(const ws_attn_desc* desc, void* cuda_stream) {
   g_last_error.clear();
   if (!desc) return fail(WS_TYPE, "null descriptor");
-  return ws_attn_launch(*desc, reinterpret_cast<cudaStream_t>(cuda_stream), g_last_error, g_launches);
+  return attn_entry(*desc, reinterpret_cast<cudaStream_t>(cuda_stream));
 }
 
 }  // extern "C"
