@@ -1,0 +1,441 @@
+"""Benchmark of the hot path: warp-specialized GEMM (+ FlashAttention forward) on B200.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+  (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...)
+
+Headline workload = BASELINE.json configs[1]: bf16 GEMM M = N = 8192 with the K sweep
+256..16384 (c = a . b^T, bf16 in/out, fp32 accumulate). One step = one pass of the sweep (7
+launches). Metric: TFLOP/s = sum 2*M*N*K over the sweep / device time; "value" is the whole job
+over all ranks. Multi-GPU = weak scaling by N-column shards: rank g computes the
+8192-column block g of a global M x (8192*N) product — no collective on the data path.
+Inputs (A+B >= 64 MB per launch, 256 MB at K=8192) stream from HBM; L2 is flushed between steps
+with a 256 MB write so every step starts cold.
+
+Extra keys: per-K rates, the attention path (C4 non-causal S=16K, C5 causal S=16K hdim 128/64),
+the roofline of the dominant kernel, e2e through the public API with host buffers, clocks, and
+the CPU baseline (the reference's own interpret_sequential from oracle/_ref when present).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+M_ = N_ = 8192
+K_SWEEP = [256, 512, 1024, 2048, 4096, 8192, 16384]
+METRIC = "GEMM & attention-fwd TFLOPS at 1/2/4/8 B200, % of tensor-core peak"
+WORKLOAD = ("C2: bf16 GEMM c = a.b^T, M=N=8192 (per GPU; global N = 8192*n_gpus), "
+            "K sweep 256..16384, one pass = 7 launches")
+
+
+def gemm_flops(K, M=M_, N=N_):
+    return 2.0 * M * N * K
+
+
+STEP_FLOPS = sum(gemm_flops(k) for k in K_SWEEP)
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return {"bf16": p["bf16_tflops"], "bf16_sustained": p.get("bf16_tflops_sustained", p["bf16_tflops"]),
+                "hbm": p["hbm_gbs"], "sm_max_mhz": p.get("sm_max_mhz"), "source": "measured"}
+    except Exception:
+        return {"bf16": 1590.0, "bf16_sustained": 1400.0, "hbm": 6650.0, "sm_max_mhz": 1965,
+                "source": "fallback (B200_PROFILING.md)"}
+
+
+def load_traffic():
+    """dram bytes per launch of the dominant kernel from the committed ncu --set full summary."""
+    path = os.path.join(ROOT, "profiles", "ncu_summary.json")
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return {}
+
+
+# ------------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ------------------------------------------------------------------------------------------------
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device_index: int):
+        self.dev = device_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits", "-lms", "100", "-i",
+                 str(self.dev)], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, smax, power, reasons = [], None, [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = float(f[2])
+                power.append(float(f[3]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "power_w_max": max(power) if power else None, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------------
+# CPU baseline: the reference's own interpret_sequential (oracle/_ref) or the C port (oracle/)
+# ------------------------------------------------------------------------------------------------
+class CpuSampler:
+    """Bounded sample of the same workload on the host cores: panel-local gemm.k output tiles
+    (128x256, the GPU tile) over a K slab, one per thread per round (BASELINE.md CPU plan)."""
+
+    def __init__(self, k_slab: int = 1024, threads: int | None = None):
+        import numpy as np
+
+        import oracle
+        from oracle import kernels as K
+
+        self.threads = threads or (os.cpu_count() or 1)
+        self.k_slab = k_slab
+        self.kind = "reference" if oracle.ref_available() else "port"
+        if self.kind == "reference":
+            src = K.gemm_src(128, 256, k_slab, 128, 256, 64)
+            self.kern = oracle.RefKernel(src)
+            self.inputs = self.kern.generate()
+        else:
+            self.a = oracle.generate_real("a", (128, k_slab))
+            self.b = oracle.generate_real("b", (256, k_slab))
+        self.np = np
+        self.oracle = oracle
+        self.flops_per_unit = 2.0 * 128 * 256 * k_slab
+
+    def _unit(self):
+        if self.kind == "reference":
+            self.kern.run(self.inputs, 0, 1)
+        else:
+            self.oracle.gemm(self.a, self.b, threads=1)
+
+    def round(self) -> float:
+        """All threads run one unit each; returns wall seconds."""
+        ths = [threading.Thread(target=self._unit) for _ in range(self.threads)]
+        t0 = time.perf_counter()
+        for t in ths:
+            t.start()
+        for t in ths:
+            t.join()
+        return time.perf_counter() - t0
+
+    def sample_desc(self, rounds):
+        return (f"{rounds} rounds x {self.threads} threads of one panel-local gemm.k 128x256 output tile over a "
+                f"K={self.k_slab} slab ({'oracle/_ref interpret_sequential' if self.kind == 'reference' else 'oracle C port'}); "
+                f"rate extrapolates linearly in tiles and K to the full M=N=8192 sweep")
+
+
+def cpu_baseline(budget_s: float = 12.0):
+    s = CpuSampler()
+    s.round()  # warm
+    rounds, wall = 0, 0.0
+    while wall < budget_s and rounds < 400:
+        wall += s.round()
+        rounds += 1
+    v = rounds * s.threads * s.flops_per_unit / wall / 1e12
+    return {"value": v, "unit": "TFLOP/s", "cores": s.threads, "kind": s.kind, "sample": s.sample_desc(rounds),
+            "wall_s": round(wall, 3)}
+
+
+def run_reference_arm(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    s = CpuSampler()
+    # size each step so the whole run stays within a few minutes
+    t1 = s.round()
+    budget = 150.0
+    per_step = budget / max(1, args.steps + args.warmup)
+    rounds_per_step = max(1, int(per_step / max(t1, 1e-3)))
+    for _ in range(args.warmup):
+        for _ in range(rounds_per_step):
+            s.round()
+    times = []
+    for _ in range(args.steps):
+        t = 0.0
+        for _ in range(rounds_per_step):
+            t += s.round()
+        times.append(t)
+    total = sum(times)
+    flops = args.steps * rounds_per_step * s.threads * s.flops_per_unit
+    value = flops / total / 1e12
+    line = {
+        "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generate_inputs)",
+        "impl": "reference",
+        "config": {"workload": WORKLOAD, "sample_per_step": f"{rounds_per_step} rounds x {s.threads} threads"},
+        "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": s.threads, "kind": s.kind,
+                         "sample": s.sample_desc(rounds_per_step * args.steps)},
+        "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------------
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2510_14719_b200 as ws
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    ws._lib.load()
+    stream = torch.cuda.current_stream()
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    Kmax = max(K_SWEEP)
+    # A and this rank's 8192-row block of B (the N-column shard); per-K operands are column slices
+    a_full = (torch.randn(M_, Kmax, device=dev, generator=g) * 0.5).to(torch.bfloat16)
+    b_full = (torch.randn(N_, Kmax, device=dev, generator=g) * 0.5).to(torch.bfloat16)
+    ops = {K: (a_full[:, :K].contiguous(), b_full[:, :K].contiguous()) for K in K_SWEEP}
+    del a_full, b_full
+    c = torch.empty(M_, N_, device=dev, dtype=torch.bfloat16)
+    flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
+
+    def step(evs=None):
+        for i, K in enumerate(K_SWEEP):
+            a, b = ops[K]
+            if evs is not None:
+                evs[i][0].record(stream)
+            ws.gemm_tn(a, b, c)
+            if evs is not None:
+                evs[i][1].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+        flush.zero_()
+    torch.cuda.synchronize()
+
+    # ---- timed region: K steps, device time, L2 flushed between steps (flush time excluded) ----
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    barrier()
+    torch.cuda.synchronize()
+    launches0 = ws.launch_count()
+    per_step = []
+    kern = {K: 0.0 for K in K_SWEEP}
+    for _ in range(args.steps):
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in K_SWEEP]
+        step(evs)
+        flush.zero_()
+        per_step.append(evs)
+    torch.cuda.synchronize()
+    launches = ws.launch_count() - launches0
+    barrier()
+    clocks = sampler.stop()
+    total_ms = 0.0
+    for evs in per_step:
+        for i, K in enumerate(K_SWEEP):
+            d = evs[i][0].elapsed_time(evs[i][1])
+            kern[K] += d
+            total_ms += d
+    total_ms = max_over_ranks(total_ms)
+    ms_per_step = total_ms / args.steps
+    value = world * STEP_FLOPS / (ms_per_step * 1e-3) / 1e12
+    per_k = {str(K): round(gemm_flops(K) / (kern[K] / args.steps * 1e-3) / 1e12, 1) for K in K_SWEEP}
+
+    peaks = load_peaks()
+    # dominant kernel: the K=16384 launch (largest share of the step)
+    Kd = max(K_SWEEP, key=lambda K: kern[K])
+    dom_ms = kern[Kd] / args.steps
+    achieved = gemm_flops(Kd) / (dom_ms * 1e-3) / 1e12
+    traffic = load_traffic().get(f"gemm_bf16_8192x8192x{Kd}", {}).get("dram_bytes_per_launch")
+    roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peaks["bf16_sustained"],
+                "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_sustained"], 4), "traffic": traffic,
+                "kernel": f"ws_gemm_tn_kernel<bf16,bf16,256> M=N=8192 K={Kd}",
+                "peak_kind": f"bf16_tflops_sustained ({peaks['source']}); the timed loop runs back to back",
+                "frac_of_burst": round(achieved / peaks["bf16"], 4),
+                "frac_of_dense_2250": round(achieved / 2250.0, 4),
+                "share_of_step": round(dom_ms / ms_per_step, 3)}
+
+    # ---- attention path (C4 / C5), reported beside the headline ----
+    attn = bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier)
+
+    # ---- e2e through the public API with host buffers (pinned), copies inside the timed region ----
+    e2e = bench_e2e(ws, torch, dev, stream, args, world, max_over_ranks, barrier)
+
+    line = {
+        "metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (randn*0.5, bf16)",
+        "config": {"workload": WORKLOAD, "M": M_, "N_per_gpu": N_, "K_sweep": K_SWEEP,
+                   "parallelism": f"N-column shards x{world} (weak)", "tile": "128x256x64 1-CTA, D=4 stages",
+                   "l2": "flushed between steps (256 MB write, excluded from timing); operands >= 64 MB per launch"},
+        "frac_of_peak": round(value / world / peaks["bf16_sustained"], 4),
+        "tflops_per_k": per_k,
+        "gemm_8192_cubed_tflops": per_k["8192"],
+        "attention": attn,
+        "roofline": roofline,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    if world == 1 and rank == 0 and not args.no_cpu_baseline:
+        try:
+            line["cpu_baseline"] = cpu_baseline()
+        except Exception as e:  # the baseline is reported, never required for the GPU number
+            line["cpu_baseline"] = {"value": None, "unit": "TFLOP/s", "cores": 0, "kind": "port",
+                                    "sample": f"unavailable: {e}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier):
+    out = {}
+    cases = [("c4_noncausal_s16k_d128", 1, 16, 16384, 128, False),
+             ("c5_causal_s16k_d128", 1, 16, 16384, 128, True),
+             ("c5_causal_s16k_d64", 1, 16, 16384, 64, True),
+             ("c4_noncausal_s1k_d128_b16", 16, 16, 1024, 128, False)]
+    iters = max(3, min(args.steps, 20))
+    for name, B, H, S, Dh, causal in cases:
+        q = torch.randn(B, H, S, Dh, device=dev, dtype=torch.bfloat16)
+        k = torch.randn_like(q)
+        v = torch.randn_like(q)
+        o = torch.empty_like(q)
+        lse = torch.empty(B, H, S, device=dev)
+        for _ in range(3):
+            ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1) / iters)
+        fl = 4.0 * B * H * S * S * Dh / (2 if causal else 1)
+        out[name] = {"tflops": round(world * fl / (ms * 1e-3) / 1e12, 1), "ms": round(ms, 4),
+                     "frac_of_peak": round(fl / (ms * 1e-3) / 1e12 / load_peaks()["bf16_sustained"], 4)}
+        del q, k, v, o, lse
+    return out
+
+
+def bench_e2e(ws, torch, dev, stream, args, world, max_over_ranks, barrier):
+    """Same sweep through ws.gemm_tn with host inputs: every step copies A, B (pinned) H2D, runs
+    the sweep and copies each C back D2H, all inside the timed region."""
+    host_ab = {}
+    for K in K_SWEEP:
+        a = (torch.randn(M_, K) * 0.5).to(torch.bfloat16).pin_memory()
+        b = (torch.randn(N_, K) * 0.5).to(torch.bfloat16).pin_memory()
+        host_ab[K] = (a, b)
+    host_c = torch.empty(M_, N_, dtype=torch.bfloat16).pin_memory()
+    dev_ab = {K: (torch.empty(M_, K, device=dev, dtype=torch.bfloat16),
+                  torch.empty(N_, K, device=dev, dtype=torch.bfloat16)) for K in K_SWEEP}
+    c = torch.empty(M_, N_, device=dev, dtype=torch.bfloat16)
+
+    def step():
+        for K in K_SWEEP:
+            da, db = dev_ab[K]
+            ha, hb = host_ab[K]
+            da.copy_(ha, non_blocking=True)
+            db.copy_(hb, non_blocking=True)
+            ws.gemm_tn(da, db, c)
+            host_c.copy_(c, non_blocking=True)
+
+    iters = max(2, min(args.steps, 10))
+    for _ in range(2):
+        step()
+    barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(iters):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1) / iters)
+    h2d = sum(2 * (M_ * K) * 2 for K in K_SWEEP)
+    d2h = len(K_SWEEP) * M_ * N_ * 2
+    return {"value": round(world * STEP_FLOPS / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3),
+            "path": "paper_2510_14719_b200.gemm_tn -> ws_gemm_tn (C-ABI) with pinned host buffers, copies on the "
+                    "launch stream"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference_arm(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

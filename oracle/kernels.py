@@ -4,7 +4,7 @@ inputs, the analogue of the reference fixtures (ref proj/tests/support/fixtures.
 
 gemm_src      — real-valued gemm.k (ref proj/kernels/gemm.k:2-17): c = a . b^T, pid column-major
                 over TM x TN output tiles (pm = pid mod TM, pn = pid div TM).
-gemm_int_src  — the shipped integer form (same shape as the reference fixture gemm_tiled_src).
+gemm_src(elem="int") — the shipped integer form (the reference fixture gemm_tiled_src shape).
 flash_src     — FlashAttention forward of SURVEY.md Appendix A (batched over B*H slices, causal via
                 the mask bank `mb`), emitting acc, row sum l and running max m.
 """
@@ -128,3 +128,46 @@ def flash_mask_bank(BR: int):
                 mb[r, BC + c] = -1e7
     mb[:, 2 * BC:] = -1e7
     return mb
+
+
+def flash_block_src(S: int, D: int, BR: int, scale: float | None = None) -> str:
+    """Panel-local flash .k: ONE BR-row query block against S keys (q is only BR rows), the unit
+    the CPU baseline times so per-pid whole-buffer copies (ref interp.hpp:140-154) do not
+    dominate (CPU baseline plan)."""
+    BC = BR
+    sc = scale if scale is not None else 1.0 / math.sqrt(D)
+    return "\n".join([
+        f"kernel flash_block(q: buf<{BR}x{D} real>, k: buf<{S}x{D} real>, v: buf<{S}x{D} real>, "
+        f"o: buf<{BR}x{D} real>, lsum: buf<{BR}x1 real>, mx: buf<{BR}x1 real>) {{",
+        f"  %zacc = const zeros : {BR}x{D} real",
+        f"  %zc = const zeros : {BR}x1 real",
+        "  %ninf = const [[-1000000.0]] : 1x1 real",
+        "  %m0 = ew add %zc, %ninf",
+        f"  %sc = const [[{sc!r}]] : 1x1 real",
+        "  %k0 = const 0",
+        f"  %zs = const zeros : {BR}x{BC} real",
+        f"  loop %j in 0..{S // BC} iter (%acc = %zacc, %m = %m0, %l = %zc, %ok = %k0) {{",
+        f"    %tq = tma_load q[0, 0] : {BR}x{D} real",
+        f"    %tk = tma_load k[%ok, 0] : {BC}x{D} real",
+        "    %s = dot %tq, %tk.T, acc=%zs",
+        f"    %tv = tma_load v[%ok, 0] : {BC}x{D} real",
+        "    %ss = ew mul %s, %sc",
+        "    %rm = reduce max %ss axis=1",
+        "    %mn = ew max %m, %rm",
+        "    %d = ew sub %ss, %mn",
+        "    %pp = ew exp %d",
+        "    %dm = ew sub %m, %mn",
+        "    %al = ew exp %dm",
+        "    %rs = reduce add %pp axis=1",
+        "    %la = ew mul %l, %al",
+        "    %l1 = ew add %la, %rs",
+        "    %as = ew mul %acc, %al",
+        "    %acc1 = dot %pp, %tv, acc=%as",
+        f"    %ok1 = add %ok, {BC}",
+        "    yield %acc1, %mn, %l1, %ok1",
+        "  }",
+        "  store o[0, 0] = %acc",
+        "  store lsum[0, 0] = %l",
+        "  store mx[0, 0] = %m",
+        "}",
+    ]) + "\n"

@@ -107,14 +107,6 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   using namespace ws;
   const int in_dt = d.in_dtype, out_dt = d.out_dtype;
   const int kbox = 128 / elem_bytes(in_dt);
-  CUtensorMap ta, tb, tc;
-  ws_status s;
-  if ((s = make_tmap(&ta, d.A, in_dt, d.M, d.K, d.lda, GEMM_BM, kbox, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
-    return s;
-  if ((s = make_tmap(&tb, d.B, in_dt, d.N, d.K, d.ldb, BN, kbox, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
-    return s;
-  const int cw = 128 / elem_bytes(out_dt);
-  if ((s = make_tmap(&tc, d.C, out_dt, d.M, d.N, d.ldc, 32, cw, CU_TENSOR_MAP_L2_PROMOTION_NONE)) != WS_OK) return s;
 
   GemmParams p;
   p.M = (int)d.M;
@@ -138,6 +130,15 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   p.group_m = d.group_m > 0 ? d.group_m : 16;
   if (p.group_m > p.num_m_blocks) p.group_m = p.num_m_blocks;
   p.scale = d.scale_a * d.scale_b;
+
+  CUtensorMap ta, tb, tc;
+  ws_status s;
+  if ((s = make_tmap(&ta, d.A, in_dt, d.M, d.K, d.lda, GEMM_BM, kbox, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
+    return s;
+  if ((s = make_tmap(&tb, d.B, in_dt, d.N, d.K, d.ldb, BN, kbox, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
+    return s;
+  const int cw = 128 / elem_bytes(out_dt);
+  if ((s = make_tmap(&tc, d.C, out_dt, d.M, d.N, d.ldc, 32, cw, CU_TENSOR_MAP_L2_PROMOTION_NONE)) != WS_OK) return s;
 
   auto kern = ws_gemm_tn_kernel<IN, OUT, BN>;
   WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
@@ -179,11 +180,6 @@ ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stre
   using namespace ws;
   const int dt = d.dtype;
   const int64_t rows = (int64_t)d.B * d.H * d.S;
-  CUtensorMap tq, tk, tv;
-  ws_status s;
-  if ((s = make_tmap(&tq, d.Q, dt, rows, DH, DH, ATTN_BM, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
-  if ((s = make_tmap(&tk, d.K, dt, rows, DH, DH, ATTN_BN, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
-  if ((s = make_tmap(&tv, d.V, dt, rows, DH, DH, ATTN_BN, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
   AttnParams p;
   p.S = d.S;
   p.Dh = DH;
@@ -204,6 +200,11 @@ ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stre
   if (p.kv_stages > ATTN_MAX_KV_STAGES || (int)smem > SMEM_LIMIT)
     return fail(WS_SMEM_OVERFLOW, "D=" + std::to_string(p.kv_stages) + " K/V stages need " + std::to_string(smem) +
                                       " B of shared memory; limit " + std::to_string(SMEM_LIMIT));
+  CUtensorMap tq, tk, tv;
+  ws_status s;
+  if ((s = make_tmap(&tq, d.Q, dt, rows, DH, DH, ATTN_BM, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
+  if ((s = make_tmap(&tk, d.K, dt, rows, DH, DH, ATTN_BN, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
+  if ((s = make_tmap(&tv, d.V, dt, rows, DH, DH, ATTN_BN, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
   auto kern = ws_attn_fwd_kernel<DH, BF16>;
   WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};

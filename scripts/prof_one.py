@@ -1,0 +1,28 @@
+"""Launch one hot-path kernel a few times (for ncu captures under gpurun)."""
+import argparse, os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2510_14719_b200 as ws
+
+ap = argparse.ArgumentParser()
+ap.add_argument("what", choices=["gemm", "gemm_fp8", "attn", "attn_causal", "attn_causal64"])
+ap.add_argument("--K", type=int, default=16384)
+ap.add_argument("--n", type=int, default=3)
+ap.add_argument("--bn", type=int, default=0)
+ap.add_argument("--D", type=int, default=0)
+ap.add_argument("--P", type=int, default=0)
+a = ap.parse_args()
+dev = torch.device("cuda")
+if a.what.startswith("gemm"):
+    dt = torch.float8_e4m3fn if a.what == "gemm_fp8" else torch.bfloat16
+    A = torch.randn(8192, a.K, device=dev).to(dt); B = torch.randn(8192, a.K, device=dev).to(dt)
+    C = torch.empty(8192, 8192, device=dev, dtype=torch.bfloat16)
+    for _ in range(a.n):
+        ws.gemm_tn(A, B, C, bn=a.bn, D=a.D, P=a.P)
+else:
+    Dh = 64 if a.what == "attn_causal64" else 128
+    q = torch.randn(1, 16, 16384, Dh, device=dev, dtype=torch.bfloat16); k = torch.randn_like(q); v = torch.randn_like(q)
+    for _ in range(a.n):
+        ws.attn_fwd(q, k, v, causal=a.what != "attn", D=a.D)
+torch.cuda.synchronize()
+print("done", a)

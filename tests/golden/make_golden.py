@@ -1,0 +1,57 @@
+"""Generate the golden vectors in this directory from the REFERENCE ITSELF.
+
+Runs the reference's own parse_kernel / generate_inputs / interpret_sequential (compiled from
+/root/reference by oracle/Makefile into oracle/_ref/libwsref.so) on small `.k` instances of the hot
+path and stores inputs and outputs as .npz. Only runnable where /root/reference exists; the
+fixtures are committed so the CPU tests can pin the oracle restatement anywhere.
+
+  python tests/golden/make_golden.py
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+
+import oracle  # noqa: E402
+from oracle import kernels as K  # noqa: E402
+
+CASES = {
+    # name: (kernel text, seed, pid count, extra fixed inputs)
+    "gemm_real_64x48x96": (K.gemm_src(64, 48, 96, 32, 16, 32), 2026, K.gemm_tiles(64, 48, 32, 16), {}),
+    "gemm_real_128x128x256": (K.gemm_src(128, 128, 256, 64, 64, 64), 2026, K.gemm_tiles(128, 128, 64, 64), {}),
+    "gemm_real_scaled_64x64x128": (K.gemm_src(64, 64, 128, 32, 32, 32, scale=0.25), 2026,
+                                   K.gemm_tiles(64, 64, 32, 32), {}),
+    "gemm_int_32x32x32": (K.gemm_src(32, 32, 32, 8, 8, 8, elem="int"), 2026, 16, {}),
+    "gemm_int_seed7_16x16x24": (K.gemm_src(16, 16, 24, 8, 8, 8, elem="int"), 7, 4, {}),
+    "flash_bh3_s64_d16": (K.flash_src(3, 64, 16, 16, causal=False), 2026, 3 * 4, {"mb": K.flash_mask_bank(16)}),
+    "flash_causal_bh3_s64_d16": (K.flash_src(3, 64, 16, 16, causal=True), 2026, 3 * 4,
+                                 {"mb": K.flash_mask_bank(16)}),
+    "flash_bh2_s128_d32": (K.flash_src(2, 128, 32, 32, causal=False), 2026, 2 * 4, {"mb": K.flash_mask_bank(32)}),
+    "flash_causal_bh2_s128_d32": (K.flash_src(2, 128, 32, 32, causal=True), 2026, 2 * 4,
+                                  {"mb": K.flash_mask_bank(32)}),
+}
+
+
+def main() -> None:
+    for name, (src, seed, pids, extra) in CASES.items():
+        rk = oracle.RefKernel(src)
+        ins = rk.generate(seed)
+        ins.update(extra)
+        out = rk.run(ins, 0, pids)
+        payload = {f"in_{k}": v for k, v in ins.items()}
+        payload.update({f"out_{k}": v for k, v in out.items()})
+        payload["kernel"] = np.array(src)
+        payload["seed"] = np.array(seed)
+        payload["pids"] = np.array(pids)
+        path = os.path.join(HERE, name + ".npz")
+        np.savez_compressed(path, **payload)
+        print(f"wrote {path}")
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,110 @@
+"""The C-ABI library (no GPU needed): it loads, exports every symbol include/ws.h declares, and
+rejects bad launches with the reference's error codes before touching the device."""
+from __future__ import annotations
+
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def _declared_functions():
+    text = open(os.path.join(ROOT, "include", "ws.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:const\s+)?[a-z_0-9]+\s*\*?\s*(ws_[a-z_0-9]+)\s*\(", text, re.M)))
+
+
+def test_header_declares_the_path():
+    assert _declared_functions() == ["ws_attn_fwd", "ws_gemm_tn", "ws_last_error", "ws_launch_count", "ws_version"]
+
+
+def test_library_exports_every_declared_symbol(ws):
+    lib = ws._lib.load()
+    for name in _declared_functions():
+        assert hasattr(lib, name), name
+    assert set(ws._lib.EXPORTS) == set(_declared_functions())
+    assert lib.ws_version().decode().startswith("ws-b200")
+    assert lib.ws_launch_count() >= 0
+
+
+def test_desc_layout_matches_header():
+    from paper_2510_14719_b200 import _lib
+
+    # in_dtype,out_dtype (8) + M,N,K (24) + A,lda,B,ldb,C,ldc (48) + scales (8) + 6 ints (24)
+    assert ctypes.sizeof(_lib.GemmDesc) == 112
+    assert ctypes.sizeof(_lib.AttnDesc) == 4 * 7 + 4 + 8 * 5 + 4 * 3 + 4  # padded to 8
+
+
+def _gemm_desc(ws, **kw):
+    d = ws._lib.GemmDesc()
+    d.in_dtype, d.out_dtype = ws._lib.WS_BF16, ws._lib.WS_F32
+    d.M, d.N, d.K = 256, 256, 256
+    d.A = d.B = d.C = 0x100000  # never dereferenced: validation fails first
+    d.lda = d.ldb = d.ldc = 256
+    d.scale_a = d.scale_b = 1.0
+    d.persistent = 1
+    for k, v in kw.items():
+        setattr(d, k, v)
+    return d
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(D=2, P=3), "pipeline-infeasible"),        # ref pipeline.hpp:84-92
+    (dict(D=-1), "pipeline-infeasible"),            # ref driver.hpp:117-118
+    (dict(M=200), "indivisible-tile"),              # ref grid.hpp:43-46
+    (dict(N=320), "indivisible-tile"),
+    (dict(K=100), "indivisible-tile"),
+    (dict(D=7), "smem-overflow"),                   # 7 x 48 KB stages > 227 KB
+    (dict(in_dtype=0), "type"),                     # fp32 inputs are not a tensor-core kind here
+    (dict(bn=96), "type"),
+    (dict(lda=128), "type"),
+])
+def test_gemm_validation_codes(ws, kw, code):
+    lib = ws._lib.load()
+    st = lib.ws_gemm_tn(ctypes.byref(_gemm_desc(ws, **kw)), None)
+    assert ws._lib.STATUS_NAMES[st] == code, lib.ws_last_error()
+    assert lib.ws_last_error()
+
+
+def _attn_desc(ws, **kw):
+    d = ws._lib.AttnDesc()
+    d.dtype = ws._lib.WS_BF16
+    d.B, d.H, d.S, d.Dh = 1, 2, 512, 128
+    d.Q = d.K = d.V = d.O = 0x100000
+    for k, v in kw.items():
+        setattr(d, k, v)
+    return d
+
+
+@pytest.mark.parametrize("kw,code", [
+    (dict(S=384), "indivisible-tile"),
+    (dict(Dh=96), "unsupported-kernel"),
+    (dict(D=1), "pipeline-infeasible"),             # coarse schedule needs D >= 2 (ref pipeline.hpp:309-315)
+    (dict(D=9), "smem-overflow"),
+    (dict(dtype=3), "type"),
+    (dict(bh_begin=1, bh_end=1), "type"),
+])
+def test_attn_validation_codes(ws, kw, code):
+    lib = ws._lib.load()
+    st = lib.ws_attn_fwd(ctypes.byref(_attn_desc(ws, **kw)), None)
+    assert ws._lib.STATUS_NAMES[st] == code, lib.ws_last_error()
+
+
+def test_python_api_raises_wserror_without_cuda_tensors(ws):
+    torch = pytest.importorskip("torch")
+    a = torch.zeros(128, 64, dtype=torch.bfloat16)
+    with pytest.raises(ws.WsError) as e:
+        ws.gemm_tn(a, a)
+    assert e.value.code == "type"
+
+
+def test_product_package_never_imports_the_oracle():
+    pkg = os.path.join(ROOT, "paper_2510_14719_b200")
+    for dirpath, _, files in os.walk(pkg):
+        for f in files:
+            if f.endswith((".py", ".cu", ".cuh", ".h")):
+                src = open(os.path.join(dirpath, f)).read()
+                assert "import oracle" not in src and "from oracle" not in src, f
+                assert "liboracle" not in src and "libwsref" not in src, f

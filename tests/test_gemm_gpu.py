@@ -1,0 +1,153 @@
+"""GEMM parity on the B200 through the C-ABI vs the CPU oracle (gemm.k, ref proj/kernels/gemm.k:2-17).
+
+Bar (BASELINE.json north_star / SURVEY.md §8c):
+  * fp32 output: BIT-EXACT. Reference inputs are k/4 with |k| <= 16, so every partial sum is a
+    multiple of 1/16 below 2^20 and any fp32 summation order equals the double oracle.
+  * bf16/fp16 output: max|d|/max|ref| <= 1e-2.      * FP8 e4m3 (scaled): <= 5e-2.
+"""
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2510_14719_b200 import shard
+from tests.gpu_helpers import as_f64, ref_tensor, rel_err
+
+pytestmark = pytest.mark.gpu
+
+F16, BF16, E4M3, F32 = torch.float16, torch.bfloat16, torch.float8_e4m3fn, torch.float32
+
+
+def _run(ws, dev, M, N, K, dt, out_dt, seed=oracle.SEED, **kw):
+    a = ref_tensor("a", (M, K), dt, dev, seed)
+    b = ref_tensor("b", (N, K), dt, dev, seed)
+    c = ws.gemm_tn(a, b, out_dtype=out_dt, **kw)
+    torch.cuda.synchronize()
+    return a, b, c
+
+
+def _want(M, N, K, seed=oracle.SEED, scale=1.0, rows=None):
+    a = oracle.generate_real("a", (M, K), seed)
+    b = oracle.generate_real("b", (N, K), seed)
+    if rows is not None:
+        a = a[rows]
+    return oracle.gemm(a, b, scale=scale)
+
+
+def test_c1_fp16_1024_cubed_bit_exact(ws, dev):
+    """C1: fp16 GEMM M=N=K=1024, fp32 accumulate — the config the CPU oracle runs in full."""
+    _, _, c = _run(ws, dev, 1024, 1024, 1024, F16, F32)
+    assert np.array_equal(as_f64(c), _want(1024, 1024, 1024))
+
+
+@pytest.mark.parametrize("dt", [F16, BF16, E4M3])
+@pytest.mark.parametrize("shape", [(128, 256, 128), (256, 512, 1024), (384, 768, 2048)])
+def test_fp32_out_bit_exact(ws, dev, dt, shape):
+    M, N, K = shape
+    _, _, c = _run(ws, dev, M, N, K, dt, F32)
+    assert np.array_equal(as_f64(c), _want(M, N, K))
+
+
+@pytest.mark.parametrize("dt,out_dt", [(BF16, BF16), (F16, F16), (BF16, F16), (E4M3, BF16)])
+def test_low_precision_out_within_tolerance(ws, dev, dt, out_dt):
+    M, N, K = 512, 512, 1024
+    _, _, c = _run(ws, dev, M, N, K, dt, out_dt)
+    assert rel_err(as_f64(c), _want(M, N, K)) <= 1e-2
+
+
+def test_fp8_per_tensor_scales(ws, dev):
+    """C3 semantics: c = (sa*sb) * a.b^T (the .k's %o = ew mul %acc, %s), tol 5e-2."""
+    M, N, K = 512, 768, 2048
+    _, _, c = _run(ws, dev, M, N, K, E4M3, BF16, scale_a=0.5, scale_b=2.0 ** -3)
+    assert rel_err(as_f64(c), _want(M, N, K, scale=0.5 * 2.0 ** -3)) <= 5e-2
+    _, _, c32 = _run(ws, dev, M, N, K, E4M3, F32, scale_a=0.5, scale_b=2.0)
+    assert np.array_equal(as_f64(c32), _want(M, N, K, scale=1.0))  # power-of-two scales stay exact
+
+
+@pytest.mark.parametrize("D", [1, 2, 3, 4])
+def test_aref_depth_and_mma_depth_sweep(ws, dev, D):
+    """Every (D, P <= D) pipeline computes the same bits (ref pipeline.hpp:44-142)."""
+    M, N, K = 256, 512, 1024
+    want = _want(M, N, K)
+    for P in range(1, D + 1):
+        _, _, c = _run(ws, dev, M, N, K, BF16, F32, D=D, P=P)
+        assert np.array_equal(as_f64(c), want), (D, P)
+
+
+def test_p_greater_than_d_is_rejected(ws, dev):
+    a = torch.zeros(128, 64, dtype=BF16, device=dev)
+    with pytest.raises(ws.WsError) as e:
+        ws.gemm_tn(a, a, D=2, P=3)
+    assert e.value.code == "pipeline-infeasible"
+
+
+@pytest.mark.parametrize("kw", [dict(bn=128), dict(persistent=False), dict(group_m=1), dict(group_m=3),
+                                dict(bn=128, persistent=False, D=6)])
+def test_schedule_variants(ws, dev, kw):
+    M, N, K = 640, 768, 512
+    _, _, c = _run(ws, dev, M, N, K, BF16, F32, **kw)
+    assert np.array_equal(as_f64(c), _want(M, N, K))
+
+
+def test_single_tile_single_kblock(ws, dev):
+    _, _, c = _run(ws, dev, 128, 256, 64, BF16, F32)
+    assert np.array_equal(as_f64(c), _want(128, 256, 64))
+
+
+def test_long_k(ws, dev):
+    _, _, c = _run(ws, dev, 256, 256, 16384, BF16, F32)
+    assert np.array_equal(as_f64(c), _want(256, 256, 16384))
+
+
+@pytest.mark.parametrize("world", [2, 4, 8])
+def test_n_column_shards_cover_the_output(ws, dev, world):
+    """rank g computes columns [n_lo, n_hi) from B rows [n_lo, n_hi) into a column
+    slice of C (ldc = N); the union of the shards equals the unsharded product."""
+    M, N, K = 256, 2048, 512
+    a = ref_tensor("a", (M, K), BF16, dev)
+    b = ref_tensor("b", (N, K), BF16, dev)
+    c = torch.full((M, N), float("nan"), dtype=F32, device=dev)
+    for r in range(world):
+        lo, hi = shard.gemm_shard(N, world, r)
+        ws.gemm_tn(a, b[lo:hi], out=c[:, lo:hi])
+    torch.cuda.synchronize()
+    assert np.array_equal(as_f64(c), _want(M, N, K))
+
+
+@pytest.mark.parametrize("K", [256, 8192])
+def test_full_size_8192_sampled_rows_exact(ws, dev, K):
+    """C2 at full size: every row checked for the size-independent row-sum identity
+    sum_n c[m,n] = a[m,:] . (sum_n b[n,:]), and 24 sampled rows (first/last of tiles and groups)
+    bit-exact against the oracle."""
+    M = N = 8192
+    a = ref_tensor("a", (M, K), BF16, dev)
+    b = ref_tensor("b", (N, K), BF16, dev)
+    c = ws.gemm_tn(a, b, out_dtype=F32)
+    torch.cuda.synchronize()
+    rowsum = c.double().sum(1)
+    want_rowsum = a.double() @ b.double().sum(0)
+    assert torch.equal(rowsum, want_rowsum)  # exact: all terms are multiples of 1/16 well below 2^53
+    rows = np.array([0, 1, 127, 128, 255, 2047, 2048, 4095, 4096, 6143, 8063, 8064, 8191]
+                    + list(np.random.default_rng(K).integers(0, M, 11)))
+    want = _want(M, N, K, rows=rows)
+    got = as_f64(c[torch.from_numpy(rows).to(dev)])
+    assert np.array_equal(got, want)
+
+
+def test_full_size_bf16_out_bench_config(ws, dev):
+    """The bench configuration (bf16 in/out, 8192^3) on sampled rows, tol 1e-2."""
+    M = N = K = 8192
+    a = ref_tensor("a", (M, K), BF16, dev)
+    b = ref_tensor("b", (N, K), BF16, dev)
+    c = ws.gemm_tn(a, b)
+    torch.cuda.synchronize()
+    rows = np.array([0, 4097, 8191])
+    assert rel_err(as_f64(c[torch.from_numpy(rows).to(dev)]), _want(M, N, K, rows=rows)) <= 1e-2
+
+
+def test_launches_are_counted(ws, dev):
+    n0 = ws.launch_count()
+    _run(ws, dev, 128, 256, 64, BF16, F32)
+    assert ws.launch_count() == n0 + 1
