@@ -102,7 +102,7 @@ int num_sms() {
 
 constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA on sm_100a
 
-template <int IN, int OUT, int BN>
+template <int IN, int OUT, int BN, int CG>
 ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   using namespace ws;
   const int in_dt = d.in_dtype, out_dt = d.out_dtype;
@@ -115,7 +115,7 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   p.num_m_blocks = (int)(d.M / GEMM_BM);
   p.num_n_blocks = (int)(d.N / BN);
   p.num_k_blocks = (int)(d.K / kbox);
-  const GemmSmemLayout L1 = gemm_smem_layout(BN, 1);
+  const GemmSmemLayout L1 = gemm_smem_layout(BN / CG, 1);
   int max_stages = (SMEM_LIMIT - (int)(L1.total - L1.stage_bytes)) / (int)L1.stage_bytes;
   if (max_stages > GEMM_MAX_STAGES) max_stages = GEMM_MAX_STAGES;
   p.stages = d.D > 0 ? d.D : max_stages;
@@ -123,32 +123,43 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   if (p.mma_depth > p.stages)
     return fail(WS_PIPELINE_INFEASIBLE, "MMA pipelining depth P=" + std::to_string(p.mma_depth) +
                                             " exceeds aref depth D=" + std::to_string(p.stages));
-  const GemmSmemLayout L = gemm_smem_layout(BN, p.stages);
+  const GemmSmemLayout L = gemm_smem_layout(BN / CG, p.stages);
   if (p.stages > GEMM_MAX_STAGES || (int)L.total > SMEM_LIMIT)
     return fail(WS_SMEM_OVERFLOW, "D=" + std::to_string(p.stages) + " stages need " + std::to_string(L.total) +
                                       " B of shared memory; limit " + std::to_string(SMEM_LIMIT));
-  p.group_m = d.group_m > 0 ? d.group_m : 16;
-  if (p.group_m > p.num_m_blocks) p.group_m = p.num_m_blocks;
+  // raster groups are counted in scheduling M-blocks (256 rows for a CTA pair)
+  p.group_m = d.group_m > 0 ? d.group_m : 16 / CG;
+  if (p.group_m > p.num_m_blocks / CG) p.group_m = p.num_m_blocks / CG;
   p.scale = d.scale_a * d.scale_b;
 
   CUtensorMap ta, tb, tc;
   ws_status s;
   if ((s = make_tmap(&ta, d.A, in_dt, d.M, d.K, d.lda, GEMM_BM, kbox, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
     return s;
-  if ((s = make_tmap(&tb, d.B, in_dt, d.N, d.K, d.ldb, BN, kbox, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
+  if ((s = make_tmap(&tb, d.B, in_dt, d.N, d.K, d.ldb, BN / CG, kbox, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
     return s;
   const int cw = 128 / elem_bytes(out_dt);
   if ((s = make_tmap(&tc, d.C, out_dt, d.M, d.N, d.ldc, 32, cw, CU_TENSOR_MAP_L2_PROMOTION_NONE)) != WS_OK) return s;
 
-  auto kern = ws_gemm_tn_kernel<IN, OUT, BN>;
+  auto kern = ws_gemm_tn_kernel<IN, OUT, BN, CG>;
   WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
-  const int tiles = p.num_m_blocks * p.num_n_blocks;
-  int grid = d.persistent ? (tiles < num_sms() ? tiles : num_sms()) : tiles;
+  const int tiles = (p.num_m_blocks / CG) * p.num_n_blocks;
+  const int units = num_sms() / CG;  // persistent: one CTA (pair) per SM (pair)
+  int grid = CG * (d.persistent ? (tiles < units ? tiles : units) : tiles);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(GEMM_THREADS);
   cfg.dynamicSmemBytes = L.total;
   cfg.stream = stream;
+  cudaLaunchAttribute attr[1];
+  if (CG == 2) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+  }
   WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return WS_OK;
@@ -156,10 +167,18 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
 
 template <int IN, int BN>
 ws_status dispatch_out(const ws_gemm_desc& d, cudaStream_t st) {
-  switch (d.out_dtype) {
-    case WS_F32: return launch_gemm<IN, ws::OUT_F32, BN>(d, st);
-    case WS_BF16: return launch_gemm<IN, ws::OUT_BF16, BN>(d, st);
-    case WS_F16: return launch_gemm<IN, ws::OUT_F16, BN>(d, st);
+  if (d.cta_pair) {
+    switch (d.out_dtype) {
+      case WS_F32: return launch_gemm<IN, ws::OUT_F32, BN, 2>(d, st);
+      case WS_BF16: return launch_gemm<IN, ws::OUT_BF16, BN, 2>(d, st);
+      case WS_F16: return launch_gemm<IN, ws::OUT_F16, BN, 2>(d, st);
+    }
+  } else {
+    switch (d.out_dtype) {
+      case WS_F32: return launch_gemm<IN, ws::OUT_F32, BN, 1>(d, st);
+      case WS_BF16: return launch_gemm<IN, ws::OUT_BF16, BN, 1>(d, st);
+      case WS_F16: return launch_gemm<IN, ws::OUT_F16, BN, 1>(d, st);
+    }
   }
   return fail(WS_TYPE, "out_dtype must be F32, BF16 or F16");
 }
@@ -256,8 +275,8 @@ ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
   if (eb == 0 || d.in_dtype == WS_F32) return fail(WS_TYPE, "in_dtype must be F16, BF16 or E4M3");
   int bn = d.bn > 0 ? d.bn : 256;
   if (bn != 128 && bn != 256) return fail(WS_TYPE, "bn must be 128 or 256");
-  if (d.cta_pair) return fail(WS_UNSUPPORTED_KERNEL, "cta_pair (cta_group::2) not built in this version");
-  if (d.M % ws::GEMM_BM) return fail(WS_INDIVISIBLE_TILE, "M=" + std::to_string(d.M) + " is not a multiple of 128");
+  const int bm = d.cta_pair ? 2 * ws::GEMM_BM : ws::GEMM_BM;
+  if (d.M % bm) return fail(WS_INDIVISIBLE_TILE, "M=" + std::to_string(d.M) + " is not a multiple of " + std::to_string(bm));
   if (d.N % bn) return fail(WS_INDIVISIBLE_TILE, "N=" + std::to_string(d.N) + " is not a multiple of bn=" + std::to_string(bn));
   if (d.K % (128 / eb))
     return fail(WS_INDIVISIBLE_TILE, "K=" + std::to_string(d.K) + " is not a multiple of " + std::to_string(128 / eb));

@@ -42,10 +42,11 @@ struct GemmSmemLayout {
   uint32_t a_bytes, b_bytes, stage_bytes, epi_offset, bar_offset, total;
 };
 
-__host__ __device__ inline GemmSmemLayout gemm_smem_layout(int bn, int stages) {
+// bn_local: rows of B this CTA loads per stage (BN, or BN/2 in a cta_group::2 pair)
+__host__ __device__ inline GemmSmemLayout gemm_smem_layout(int bn_local, int stages) {
   GemmSmemLayout L;
   L.a_bytes = GEMM_BM * GEMM_ROW_BYTES;
-  L.b_bytes = bn * GEMM_ROW_BYTES;
+  L.b_bytes = bn_local * GEMM_ROW_BYTES;
   L.stage_bytes = L.a_bytes + L.b_bytes;
   L.epi_offset = stages * L.stage_bytes;
   L.bar_offset = L.epi_offset + 4 * 2 * GEMM_EPI_BUF_BYTES;
@@ -56,30 +57,38 @@ __host__ __device__ inline GemmSmemLayout gemm_smem_layout(int bn, int stages) {
 
 // Tile order: grouped raster over (m, n) blocks so that a wave of CTAs shares A and B panels in
 // L2. The set of tiles equals the .k pid set {pm + pn * TM}; only the visiting order changes.
-__device__ __forceinline__ void gemm_tile_coords(int t, const GemmParams& p, int& mb, int& nb) {
+// num_m: scheduling M-blocks (128 rows, or 256 for a CTA pair).
+__device__ __forceinline__ void gemm_tile_coords(int t, const GemmParams& p, int num_m, int& mb, int& nb) {
   int per_group = p.group_m * p.num_n_blocks;
   int g = t / per_group;
   int first_m = g * p.group_m;
-  int gsize = min(p.num_m_blocks - first_m, p.group_m);
+  int gsize = min(num_m - first_m, p.group_m);
   int r = t - g * per_group;
   mb = first_m + r % gsize;
   nb = r / gsize;
 }
 
-template <int IN, int OUT, int BN>
+// CG = 1: one CTA computes a 128 x BN tile.
+// CG = 2: a cluster of two CTAs (a TPC pair) computes a 256 x BN tile with cta_group::2 MMAs
+// issued by the leader CTA: each CTA stages its own 128 rows of A and BN/2 rows of B, the tensor
+// cores read B from both CTAs, and each CTA's TMEM receives its own 128 accumulator rows. This is
+// the reference's cooperative mode (consumer row bands sharing one producer stream,
+// ref proj/include/warpspec/grid.hpp:24-72) mapped onto the SM pair.
+template <int IN, int OUT, int BN, int CG>
 __global__ void __launch_bounds__(GEMM_THREADS, 1)
     ws_gemm_tn_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_c, const GemmParams p) {
+  constexpr int BN_LOCAL = BN / CG;
   constexpr uint32_t TMEM_COLS = 2 * BN <= 256 ? 256 : 512;  // two accumulator buffers
   constexpr int OUT_BYTES = OUT == OUT_F32 ? 4 : 2;
   constexpr int CW = 128 / OUT_BYTES;  // epilogue chunk: output columns per 128-byte row
   constexpr int UMMA_K_BYTES = 32;     // 16 x 16-bit or 32 x 8-bit per tcgen05.mma
   constexpr int KSTEPS = GEMM_ROW_BYTES / UMMA_K_BYTES;
-  constexpr uint32_t IDESC = make_idesc(IN == IN_BF16 ? 1u : 0u, GEMM_BM, BN, 0, 0);
+  constexpr uint32_t IDESC = make_idesc(IN == IN_BF16 ? 1u : 0u, GEMM_BM * CG, BN, 0, 0);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const GemmSmemLayout L = gemm_smem_layout(BN, p.stages);
+  const GemmSmemLayout L = gemm_smem_layout(BN_LOCAL, p.stages);
   auto* ring = reinterpret_cast<ArefBarriers<GEMM_MAX_STAGES>*>(smem + L.bar_offset);
   uint64_t* tmem_full = reinterpret_cast<uint64_t*>(smem + L.bar_offset + 2 * GEMM_MAX_STAGES * 8);
   uint64_t* tmem_empty = tmem_full + 2;
@@ -87,8 +96,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int num_tiles = p.num_m_blocks * p.num_n_blocks;
+  const int num_tiles = (p.num_m_blocks / CG) * p.num_n_blocks;  // pair tiles when CG == 2
   const uint32_t D = static_cast<uint32_t>(p.stages);
+  const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
+  const bool leader = rank == 0;
+  const int tile0 = static_cast<int>(blockIdx.x) / CG, tile_stride = static_cast<int>(gridDim.x) / CG;
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_a);
@@ -97,15 +109,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     ring->init(D, 1, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], 4);  // one arrival per epilogue warp
+      mbar_init(&tmem_empty[i], 4 * CG);  // one arrival per epilogue warp of every CTA in the pair
     }
     fence_barrier_init();
   } else if (warp == 2) {
-    tmem_alloc<1>(tmem_base_slot, TMEM_COLS);
-    tmem_relinquish<1>();
+    tmem_alloc<CG>(tmem_base_slot, TMEM_COLS);
+    tmem_relinquish<CG>();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();  // peer barriers initialised before any remote arrive / multicast commit
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
 
@@ -113,30 +128,39 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // ===================== TMA producer: aref put =====================
     if (lane == 0) {
       ArefCursor c;
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = tile0; t < num_tiles; t += tile_stride) {
         int mb, nb;
-        gemm_tile_coords(t, p, mb, nb);
+        gemm_tile_coords(t, p, p.num_m_blocks / CG, mb, nb);
+        const int arow = mb * GEMM_BM * CG + static_cast<int>(rank) * GEMM_BM;
+        const int brow = nb * BN + static_cast<int>(rank) * BN_LOCAL;
         for (int kb = 0; kb < p.num_k_blocks; ++kb) {
           ring->put_acquire(c, 1);
-          ring->put_expect(c, L.stage_bytes);
           uint8_t* sa = smem + c.slot * L.stage_bytes;
           uint8_t* sb = sa + L.a_bytes;
           // coordinates are in elements of the tensor map's innermost dim (K) then rows
           const int kcoord = kb * (IN == IN_E4M3 ? 128 : 64);
-          tma_load_2d(sa, &tm_a, &ring->full[c.slot], kcoord, mb * GEMM_BM);
-          tma_load_2d(sb, &tm_b, &ring->full[c.slot], kcoord, nb * BN);
+          if constexpr (CG == 1) {
+            ring->put_expect(c, L.stage_bytes);
+            tma_load_2d(sa, &tm_a, &ring->full[c.slot], kcoord, arow);
+            tma_load_2d(sb, &tm_b, &ring->full[c.slot], kcoord, brow);
+          } else {
+            // the leader's full barrier collects both CTAs' bytes (one expect_tx for the pair)
+            if (leader) ring->put_expect(c, 2 * L.stage_bytes);
+            tma_load_2d_cg2(sa, &tm_a, &ring->full[c.slot], kcoord, arow);
+            tma_load_2d_cg2(sb, &tm_b, &ring->full[c.slot], kcoord, brow);
+          }
           c.advance(D);
         }
       }
     }
   } else if (warp == 1) {
     // ===================== MMA issuer: aref get / consumed =====================
-    if (lane == 0) {
+    if (lane == 0 && leader) {
       ArefCursor c;
       uint32_t gk = 0;  // global k-block counter (for the literal P window)
       uint32_t acc_stage = 0, acc_phase = 0;
       const uint32_t P = static_cast<uint32_t>(p.mma_depth);
-      for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+      for (int t = tile0; t < num_tiles; t += tile_stride) {
         mbar_wait(&tmem_empty[acc_stage], acc_phase ^ 1u, 3);
         tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc_stage * BN;
@@ -155,14 +179,21 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             const uint64_t ad = make_sw128_desc(sa + k * UMMA_K_BYTES, 16, 1024);
             const uint64_t bd = make_sw128_desc(sb + k * UMMA_K_BYTES, 16, 1024);
             if constexpr (IN == IN_E4M3)
-              mma_f8_ss<1>(d_tmem, ad, bd, IDESC, (kb | k) != 0);
+              mma_f8_ss<CG>(d_tmem, ad, bd, IDESC, (kb | k) != 0);
             else
-              mma_f16_ss<1>(d_tmem, ad, bd, IDESC, (kb | k) != 0);
+              mma_f16_ss<CG>(d_tmem, ad, bd, IDESC, (kb | k) != 0);
           }
-          ring->consumed_by_mma(c);
+          if constexpr (CG == 1)
+            ring->consumed_by_mma(c);
+          else
+            mma_commit_mc2(&ring->empty[c.slot], 0x3);  // release the slot in both CTAs
           c.advance(D);
         }
-        mma_commit(&tmem_full[acc_stage]);  // accumulator aref: put by the tensor core
+        // accumulator aref: put by the tensor core
+        if constexpr (CG == 1)
+          mma_commit(&tmem_full[acc_stage]);
+        else
+          mma_commit_mc2(&tmem_full[acc_stage], 0x3);
         if (++acc_stage == 2) {
           acc_stage = 0;
           acc_phase ^= 1u;
@@ -175,9 +206,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint8_t* stage_base = smem + L.epi_offset + q * 2 * GEMM_EPI_BUF_BYTES;
     uint32_t acc_stage = 0, acc_phase = 0, chunk_ctr = 0;
     const float scale = p.scale;
-    for (int t = blockIdx.x; t < num_tiles; t += gridDim.x) {
+    for (int t = tile0; t < num_tiles; t += tile_stride) {
       int mb, nb;
-      gemm_tile_coords(t, p, mb, nb);
+      gemm_tile_coords(t, p, p.num_m_blocks / CG, mb, nb);
+      const int crow = mb * GEMM_BM * CG + static_cast<int>(rank) * GEMM_BM;
       mbar_wait(&tmem_full[acc_stage], acc_phase, 5);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc_stage * BN;
@@ -195,7 +227,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           // accumulator fully read: release it to the MMA warp (accumulator aref consumed)
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tmem_empty[acc_stage]);
+          if (lane == 0) {
+            if constexpr (CG == 1)
+              mbar_arrive(&tmem_empty[acc_stage]);
+            else
+              mbar_arrive_cluster(&tmem_empty[acc_stage], 0);  // the leader's MMA warp owns the release
+          }
         }
         uint8_t* buf = stage_base + (chunk_ctr & 1u) * GEMM_EPI_BUF_BYTES;
         if (chunk_ctr >= 2) {
@@ -233,7 +270,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&tm_c, buf, nb * BN + ch * CW, mb * GEMM_BM + q * 32);
+          tma_store_2d(&tm_c, buf, nb * BN + ch * CW, crow + q * 32);
           tma_store_commit();
         }
       }
@@ -246,10 +283,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   }
 
   tc_fence_before();
-  __syncthreads();
+  if constexpr (CG == 2)
+    cluster_sync();  // the peer's TMEM is written by the leader's MMAs: free only when both are done
+  else
+    __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc<1>(tmem_base, TMEM_COLS);
+    tmem_dealloc<CG>(tmem_base, TMEM_COLS);
   }
 }
 

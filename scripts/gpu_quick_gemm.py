@@ -35,23 +35,25 @@ def bench(M, N, K, dt, out_dt, iters=20, **kw):
 
 if __name__ == "__main__":
     torch.cuda.init()
-    check(128, 256, 64, torch.bfloat16, torch.float32)
-    check(256, 512, 256, torch.bfloat16, torch.float32)
-    check(1024, 1024, 1024, torch.float16, torch.float32)
-    check(1024, 1024, 1024, torch.bfloat16, torch.bfloat16)
-    check(1024, 1024, 1024, torch.bfloat16, torch.float32, D=2, P=1)
-    check(1024, 1024, 1024, torch.bfloat16, torch.float32, bn=128)
-    check(1024, 1024, 1024, torch.bfloat16, torch.float32, persistent=False)
-    check(1024, 1024, 1024, torch.float8_e4m3fn, torch.float32)
-    check(2048, 2048, 4096, torch.float8_e4m3fn, torch.bfloat16, scale_a=0.5, scale_b=2.0)
-    check(4096, 4096, 4096, torch.bfloat16, torch.float32)
+    check(256, 256, 64, torch.bfloat16, torch.float32, cta_pair=True)
+    check(512, 512, 256, torch.bfloat16, torch.float32, cta_pair=True)
+    check(1024, 1024, 1024, torch.float16, torch.float32, cta_pair=True)
+    check(1024, 1024, 1024, torch.bfloat16, torch.float32, cta_pair=True, D=2, P=1)
+    check(1024, 1024, 1024, torch.bfloat16, torch.float32, cta_pair=True, persistent=False)
+    check(1024, 1024, 1024, torch.float8_e4m3fn, torch.float32, cta_pair=True)
+    check(2048, 2048, 4096, torch.bfloat16, torch.bfloat16, cta_pair=True)
+    check(4096, 4096, 4096, torch.bfloat16, torch.float32, cta_pair=True)
+    check(1024, 1024, 1024, torch.bfloat16, torch.float32, cta_pair=True, bn=128)
     for K in (256, 1024, 8192, 16384):
         bench(8192, 8192, K, torch.bfloat16, torch.bfloat16)
-    bench(8192, 8192, 8192, torch.bfloat16, torch.bfloat16, bn=128)
-    bench(8192, 8192, 8192, torch.float8_e4m3fn, torch.bfloat16)
+        bench(8192, 8192, K, torch.bfloat16, torch.bfloat16, cta_pair=True)
+    for gm in (4, 8, 16):
+        bench(8192, 8192, 8192, torch.bfloat16, torch.bfloat16, cta_pair=True, group_m=gm)
+    bench(8192, 8192, 8192, torch.float8_e4m3fn, torch.bfloat16, cta_pair=True)
+    bench(8192, 8192, 16384, torch.float8_e4m3fn, torch.bfloat16, cta_pair=True)
     a = torch.randn(8192, 8192, device="cuda", dtype=torch.bfloat16)
     for _ in range(3): a @ a.T
-    torch.cuda.synchronize(); t = time.time()
+    torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True); e0.record()
     for _ in range(20): a @ a.T
     e1.record(); torch.cuda.synchronize(); ms = e0.elapsed_time(e1)/20
