@@ -101,6 +101,13 @@ typedef struct ws_attn_desc {
 ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream);
 ws_status ws_attn_fwd(const ws_attn_desc* desc, void* cuda_stream);
 
+/* ws_attn_fwd plus a device trace of CTA (0,0): `trace` is a device buffer of 3*256*8 uint64
+ * %clock64 stamps — per KV step j, the MMA issuer (role 0) and the first softmax warp of each Q
+ * tile (roles 1, 2) record when they start waiting, pass each mbarrier and finish each stage.
+ * This is the hardware counterpart of the simulator's per-unit busy intervals
+ * (ref proj/include/warpspec/sim.hpp:16-36, trace.hpp:59-83); layout in csrc/attn_sm100.cuh. */
+ws_status ws_attn_fwd_traced(const ws_attn_desc* desc, void* cuda_stream, unsigned long long* trace);
+
 /* Message for the last non-OK status returned on this thread ("" if none). */
 const char* ws_last_error(void);
 

@@ -53,6 +53,7 @@ class AttnDesc(ctypes.Structure):
 EXPORTS = {
     "ws_gemm_tn": (ctypes.c_int, [ctypes.POINTER(GemmDesc), ctypes.c_void_p]),
     "ws_attn_fwd": (ctypes.c_int, [ctypes.POINTER(AttnDesc), ctypes.c_void_p]),
+    "ws_attn_fwd_traced": (ctypes.c_int, [ctypes.POINTER(AttnDesc), ctypes.c_void_p, ctypes.c_void_p]),
     "ws_last_error": (ctypes.c_char_p, []),
     "ws_launch_count": (ctypes.c_int64, []),
     "ws_version": (ctypes.c_char_p, []),

@@ -195,7 +195,7 @@ ws_status dispatch_in(const ws_gemm_desc& d, cudaStream_t st) {
 
 
 template <int DH, bool BF16>
-ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stream) {
+ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stream, unsigned long long* trace) {
   using namespace ws;
   const int dt = d.dtype;
   const int64_t rows = (int64_t)d.B * d.H * d.S;
@@ -210,7 +210,8 @@ ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stre
   p.lse = d.LSE;
   p.o = d.O;
   p.o_elem = BF16 ? 0 : 1;
-  int max_stages = (SMEM_LIMIT - (int)attn_smem_bytes(DH, 0)) / (int)attn_tile_bytes(DH);
+  p.trace = trace;
+  int max_stages = (SMEM_LIMIT - (int)attn_smem_bytes(DH, 0)) / (int)attn_kv_bytes(DH);
   if (max_stages > ATTN_MAX_KV_STAGES) max_stages = ATTN_MAX_KV_STAGES;
   p.kv_stages = d.D > 0 ? d.D : max_stages;
   if (p.kv_stages < 2)
@@ -236,7 +237,7 @@ ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stre
   return WS_OK;
 }
 
-ws_status attn_entry(const ws_attn_desc& d, cudaStream_t st) {
+ws_status attn_entry(const ws_attn_desc& d, cudaStream_t st, unsigned long long* trace) {
   if (d.dtype != WS_BF16 && d.dtype != WS_F16) return fail(WS_TYPE, "attention dtype must be BF16 or F16");
   if (d.B <= 0 || d.H <= 0 || d.S <= 0) return fail(WS_TYPE, "B, H, S must be positive");
   if (d.Dh != 64 && d.Dh != 128) return fail(WS_UNSUPPORTED_KERNEL, "head dim must be 64 or 128");
@@ -249,8 +250,10 @@ ws_status attn_entry(const ws_attn_desc& d, cudaStream_t st) {
   if (bh0 < 0 || bh1 > BH || bh0 >= bh1) return fail(WS_TYPE, "bad (b,h) shard range");
   if ((int64_t)BH * d.S >= (int64_t)1 << 31) return fail(WS_TYPE, "B*H*S must fit in int32");
   if (d.Dh == 128)
-    return d.dtype == WS_BF16 ? launch_attn<128, true>(d, bh0, bh1, st) : launch_attn<128, false>(d, bh0, bh1, st);
-  return d.dtype == WS_BF16 ? launch_attn<64, true>(d, bh0, bh1, st) : launch_attn<64, false>(d, bh0, bh1, st);
+    return d.dtype == WS_BF16 ? launch_attn<128, true>(d, bh0, bh1, st, trace)
+                              : launch_attn<128, false>(d, bh0, bh1, st, trace);
+  return d.dtype == WS_BF16 ? launch_attn<64, true>(d, bh0, bh1, st, trace)
+                            : launch_attn<64, false>(d, bh0, bh1, st, trace);
 }
 
 }  // namespace
@@ -288,7 +291,13 @@ ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
 ws_status ws_attn_fwd(const ws_attn_desc* desc, void* cuda_stream) {
   g_last_error.clear();
   if (!desc) return fail(WS_TYPE, "null descriptor");
-  return attn_entry(*desc, reinterpret_cast<cudaStream_t>(cuda_stream));
+  return attn_entry(*desc, reinterpret_cast<cudaStream_t>(cuda_stream), nullptr);
+}
+
+ws_status ws_attn_fwd_traced(const ws_attn_desc* desc, void* cuda_stream, unsigned long long* trace) {
+  g_last_error.clear();
+  if (!desc) return fail(WS_TYPE, "null descriptor");
+  return attn_entry(*desc, reinterpret_cast<cudaStream_t>(cuda_stream), trace);
 }
 
 }  // extern "C"

@@ -28,19 +28,19 @@ namespace ws {
 
 static __device__ WatchdogRecord ws_watchdog_record;
 
-static __device__ __noinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity, uint32_t tag) {
+// Out of line on purpose would force ABI register saves in the 224-register softmax regions
+// (setmaxnreg budgets are per region); the slow path is inlined and stays cold.
+static __device__ __forceinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity, uint32_t tag) {
   uint64_t t0 = globaltimer();
   uint32_t spins = 0;
   while (!mbar_try_wait(bar, parity)) {
     if (((++spins) & 1023u) == 0 && globaltimer() - t0 > WS_WATCHDOG_NS) {
-      ws_watchdog_record.block = blockIdx.x;
+      ws_watchdog_record.block = blockIdx.x | (static_cast<unsigned long long>(blockIdx.y) << 32);
       ws_watchdog_record.thread = threadIdx.x;
       ws_watchdog_record.bar_smem = bar;
       ws_watchdog_record.parity = parity;
       ws_watchdog_record.tag = tag;
       __threadfence_system();
-      printf("[ws watchdog] block %d thread %d stuck on mbarrier smem=0x%x parity=%u tag=%u\n", (int)blockIdx.x,
-             (int)threadIdx.x, bar, parity, tag);
       asm volatile("trap;");
     }
   }

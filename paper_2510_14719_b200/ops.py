@@ -32,12 +32,14 @@ def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
 
 def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None, *,
             out_dtype: Optional[torch.dtype] = None, scale_a: float = 1.0, scale_b: float = 1.0,
-            D: int = 0, P: int = 0, persistent: bool = True, cta_pair: bool = False, bn: int = 0,
+            D: int = 0, P: int = 0, persistent: bool = True, cta_pair: Optional[bool] = None, bn: int = 0,
             group_m: int = 0, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
     """c[M,N] = scale_a*scale_b * a[M,K] . b[N,K]^T with fp32 accumulation on the tensor cores.
 
     a, b: row-major (last dim contiguous) CUDA tensors of dtype f16/bf16/float8_e4m3fn.
     out: optional [M,N] tensor (may be a column slice of a wider matrix; its row stride is ldc).
+    cta_pair: None = auto (cta_group::2 CTA pairs when M % 256 == 0 and K >= 1024, where the
+    mainloop dominates; single-CTA tiles for short K, where the epilogue does).
     """
     if a.device.type != "cuda" or b.device.type != "cuda":
         raise _lib.WsError(2, "operands must be CUDA tensors (no CPU path)")
@@ -49,6 +51,8 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
         raise _lib.WsError(2, f"inner dimensions disagree: {K} vs {K2}")
     if a.stride(1) != 1 or b.stride(1) != 1:
         raise _lib.WsError(2, "operands must be K-contiguous (row-major)")
+    if cta_pair is None:
+        cta_pair = M % 256 == 0 and K >= 1024
     if out is None:
         od = out_dtype or (torch.bfloat16 if a.dtype == torch.float8_e4m3fn else a.dtype)
         out = torch.empty((M, N), dtype=od, device=a.device)
@@ -72,9 +76,12 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
 def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool = False,
              softmax_scale: Optional[float] = None, out: Optional[torch.Tensor] = None,
              lse: Optional[torch.Tensor] = None, D: int = 0, bh_range: Optional[tuple] = None,
-             stream: Optional[torch.cuda.Stream] = None):
+             stream: Optional[torch.cuda.Stream] = None, trace: Optional[torch.Tensor] = None):
     """FlashAttention forward over [B, H, S, Dh] tensors. Returns (o, lse) with lse fp32 [B, H, S]
-    in natural-log units (lse = m + log l of the .k's running max m and row sum l)."""
+    in natural-log units (lse = m + log l of the .k's running max m and row sum l).
+
+    trace: optional int64 CUDA tensor of 3*256*8 entries receiving %clock64 stamps of CTA (0,0)
+    (see ws_attn_fwd_traced in include/ws.h)."""
     if q.device.type != "cuda":
         raise _lib.WsError(2, "operands must be CUDA tensors (no CPU path)")
     if not (q.dtype == k.dtype == v.dtype) or q.dtype not in (torch.float16, torch.bfloat16):
@@ -98,7 +105,11 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool 
     lo, hi = bh_range if bh_range is not None else (0, B * H)
     d.bh_begin, d.bh_end = lo, hi
     lib = _lib.load()
-    _lib.check(lib.ws_attn_fwd(ctypes.byref(d), ctypes.c_void_p(_stream_ptr(stream))))
+    if trace is not None:
+        _lib.check(lib.ws_attn_fwd_traced(ctypes.byref(d), ctypes.c_void_p(_stream_ptr(stream)),
+                                          ctypes.c_void_p(trace.data_ptr())))
+    else:
+        _lib.check(lib.ws_attn_fwd(ctypes.byref(d), ctypes.c_void_p(_stream_ptr(stream))))
     return out, lse
 
 

@@ -49,7 +49,9 @@ if __name__ == "__main__":
     check(1, 2, 512, 64, True)
     check(2, 3, 1024, 128, False, dt=torch.float16)
     check(1, 2, 1024, 128, True, scale_in=0.25)
-    check(1, 2, 1024, 128, False, D=2)
+    for D in (2, 3, 4, 5, 6):
+        check(1, 2, 1024, 128, True, D=D)
+        check(1, 2, 1024, 64, False, D=D)
     for S in (1024, 4096, 16384):
         bench(16384 // S, 16, S, 128, False)
     bench(1, 16, 16384, 128, True)

@@ -11,6 +11,7 @@ ap.add_argument("--n", type=int, default=3)
 ap.add_argument("--bn", type=int, default=0)
 ap.add_argument("--D", type=int, default=0)
 ap.add_argument("--P", type=int, default=0)
+ap.add_argument("--cta_pair", action="store_true")
 a = ap.parse_args()
 dev = torch.device("cuda")
 if a.what.startswith("gemm"):
@@ -18,7 +19,7 @@ if a.what.startswith("gemm"):
     A = torch.randn(8192, a.K, device=dev).to(dt); B = torch.randn(8192, a.K, device=dev).to(dt)
     C = torch.empty(8192, 8192, device=dev, dtype=torch.bfloat16)
     for _ in range(a.n):
-        ws.gemm_tn(A, B, C, bn=a.bn, D=a.D, P=a.P)
+        ws.gemm_tn(A, B, C, bn=a.bn, D=a.D, P=a.P, cta_pair=a.cta_pair)
 else:
     Dh = 64 if a.what == "attn_causal64" else 128
     q = torch.randn(1, 16, 16384, Dh, device=dev, dtype=torch.bfloat16); k = torch.randn_like(q); v = torch.randn_like(q)

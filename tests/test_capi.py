@@ -17,7 +17,8 @@ def _declared_functions():
 
 
 def test_header_declares_the_path():
-    assert _declared_functions() == ["ws_attn_fwd", "ws_gemm_tn", "ws_last_error", "ws_launch_count", "ws_version"]
+    assert _declared_functions() == ["ws_attn_fwd", "ws_attn_fwd_traced", "ws_gemm_tn", "ws_last_error",
+                                    "ws_launch_count", "ws_version"]
 
 
 def test_library_exports_every_declared_symbol(ws):
