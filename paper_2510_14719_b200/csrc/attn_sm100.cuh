@@ -78,7 +78,17 @@ __host__ __device__ inline uint32_t attn_smem_bytes(int Dh, int kv_stages) {
   return 2 * attn_q_bytes(Dh) + kv_stages * attn_kv_bytes(Dh) + (2 * ATTN_MAX_KV_STAGES + 16) * 8 + 16 + 1024;
 }
 
-template <int DH, bool BF16>
+// POLY = how many of every 8 column pairs are exponentiated on the FMA pipe (exp2_poly2) instead of
+// MUFU (16 ex2/clk/SM). Measured (scripts/micro/softmax_loop.cu): 3 of 8 is the fastest mix.
+__host__ __device__ constexpr bool attn_poly_pair(int POLY, int i) {
+  return POLY == 0 ? false
+       : POLY == 2 ? (i == 1 || i == 5)
+       : POLY == 3 ? (i == 1 || i == 4 || i == 6)
+       : POLY == 4 ? (i & 1) == 1
+                   : (i != 0 && i != 3 && i != 6);
+}
+
+template <int DH, bool BF16, int POLY = 3>
 __global__ void __launch_bounds__(ATTN_THREADS, 1)
     ws_attn_fwd_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                        const __grid_constant__ CUtensorMap tm_v, const AttnParams p) {
@@ -339,7 +349,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
         for (int c = c0; c < c0 + 32; c += 2) {
           const uint64_t x2 = f2_fma(f2_pack(s[c], s[c + 1]), sl2x2, negm2);
           uint64_t p2;
-          if (((c / 2) & 7) == 1 || ((c / 2) & 7) == 4 || ((c / 2) & 7) == 6) {
+          if (attn_poly_pair(POLY, (c / 2) & 7)) {
             p2 = exp2_poly2(x2);
           } else {
             float x0, x1;

@@ -383,6 +383,25 @@ __device__ __forceinline__ uint64_t make_sw128_desc(uint32_t smem_addr, uint32_t
   return d;
 }
 
+// SWIZZLE_NONE (interleaved) K-major descriptor: core matrices of 8 rows x 16 B; LBO = byte
+// distance between the two K halves of a K=16 step, SBO = distance between 8-row groups. With
+// both 0 every core matrix aliases the same 128 bytes (used for an all-ones operand).
+__device__ __forceinline__ uint64_t make_interleave_desc(uint32_t smem_addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFFu);
+  d |= static_cast<uint64_t>((lbo_bytes >> 4) & 0x3FFFu) << 16;
+  d |= static_cast<uint64_t>((sbo_bytes >> 4) & 0x3FFFu) << 32;
+  d |= 1ull << 46;
+  return d;  // layout type 0 = SWIZZLE_NONE
+}
+
+__device__ __forceinline__ void tmem_ld1(uint32_t taddr, uint32_t& v) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(v) : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_st1(uint32_t taddr, uint32_t v) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(taddr), "r"(v) : "memory");
+}
+
 // Instruction descriptor for kind::f16 / kind::f8f6f4 with fp32 accumulation.
 //   [4,6) c_format (1 = f32), [7,10) a_format, [10,13) b_format, [15] a_major, [16] b_major,
 //   [17,23) N >> 3, [24,29) M >> 4.

@@ -49,7 +49,7 @@ if __name__ == "__main__":
     check(1, 2, 512, 64, True)
     check(2, 3, 1024, 128, False, dt=torch.float16)
     check(1, 2, 1024, 128, True, scale_in=0.25)
-    for D in (2, 3, 4, 5, 6):
+    for D in (2, 3, 4, 5):
         check(1, 2, 1024, 128, True, D=D)
         check(1, 2, 1024, 64, False, D=D)
     for S in (1024, 4096, 16384):
