@@ -80,6 +80,8 @@ typedef struct ws_gemm_desc {
   int32_t cta_pair;            /* 1 = cta_group::2 256-row tiles (cooperative WGs analogue) */
   int32_t bn;                  /* N tile: 0 = auto, else 128 or 256 */
   int32_t group_m;             /* raster: tiles grouped by this many M-blocks; 0 = auto */
+  int32_t act;                 /* epilogue activation: 0 none, 1 relu (gemm_act.k, ref
+                                  proj/kernels/gemm_act.k:10-16) */
 } ws_gemm_desc;
 
 /* FlashAttention forward. q,k,v,o: [B, H, S, Dh] contiguous; lse: [B, H, S] fp32 (natural log,
@@ -107,6 +109,25 @@ ws_status ws_attn_fwd(const ws_attn_desc* desc, void* cuda_stream);
  * This is the hardware counterpart of the simulator's per-unit busy intervals
  * (ref proj/include/warpspec/sim.hpp:16-36, trace.hpp:59-83); layout in csrc/attn_sm100.cuh. */
 ws_status ws_attn_fwd_traced(const ws_attn_desc* desc, void* cuda_stream, unsigned long long* trace);
+
+/* `.k` front end: run pids [pid_lo, pid_hi) of a kernel written in the
+ * reference grammar (ref SPEC.md:120-134) on the GPU, like the reference's tile-by-tile oracle
+ * run `interpret_tiles` (ref proj/tests/support/fixtures.hpp:148-157). Buffers are the kernel's
+ * parameters by name, as host arrays: double for `real`, int64 for `int`; in/out; parameters
+ * without a buffer start zeroed. Supported shapes: the gemm.k family (gemm / gemm_large /
+ * gemm_batched / gemm_act forms, optional 1x1 scale epilogue) — exact for the reference's payloads
+ * with device dtype BF16 — and the flash .k of SURVEY.md Appendix A (written back as o = O,
+ * lsum = 1, mx = lse, i.e. the same o/lsum and mx + log(lsum) as the .k). Anything else returns
+ * WS_UNSUPPORTED_KERNEL; grammar errors WS_PARSE. Synchronous w.r.t. the host buffers. */
+typedef struct ws_kbuffer {
+  const char* name;
+  int64_t rows, cols;
+  int32_t is_real;
+  void* data;
+} ws_kbuffer;
+
+ws_status ws_run_kernel(const char* ktext, ws_kbuffer* buffers, int32_t nbuffers, int64_t pid_lo, int64_t pid_hi,
+                        int32_t dtype, void* cuda_stream);
 
 /* Message for the last non-OK status returned on this thread ("" if none). */
 const char* ws_last_error(void);

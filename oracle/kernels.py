@@ -171,3 +171,60 @@ def flash_block_src(S: int, D: int, BR: int, scale: float | None = None) -> str:
         "  store mx[0, 0] = %m",
         "}",
     ]) + "\n"
+
+
+def gemm_batched_src(batches: int, T: int, BT: int, K: int, BK: int, elem: str = "int") -> str:
+    """gemm_batched.k shape (ref proj/kernels/gemm_batched.k:2-22): `batches` independent T x T x K
+    products stacked along rows, BT x BT tiles, pid = batch * (T/BT)^2 + tile."""
+    tpb = T // BT
+    rows = batches * T
+    return "\n".join([
+        f"kernel gemm_batched(a: buf<{rows}x{K} {elem}>, b: buf<{rows}x{K} {elem}>, c: buf<{rows}x{T} {elem}>) {{",
+        "  %p = pid",
+        f"  %bi = div %p, {tpb * tpb}",
+        f"  %t = mod %p, {tpb * tpb}",
+        f"  %tm = mod %t, {tpb}",
+        f"  %tn = div %t, {tpb}",
+        f"  %rbase = mul %bi, {T}",
+        f"  %tmr = mul %tm, {BT}",
+        f"  %tnr = mul %tn, {BT}",
+        "  %r = add %rbase, %tmr",
+        "  %rb = add %rbase, %tnr",
+        f"  %z = const zeros : {BT}x{BT} {elem}",
+        "  %k0 = const 0",
+        f"  loop %k in 0..{K // BK} iter (%acc = %z, %ok = %k0) {{",
+        f"    %ta = tma_load a[%r, %ok] : {BT}x{BK} {elem}",
+        f"    %tb = tma_load b[%rb, %ok] : {BT}x{BK} {elem}",
+        "    %acc1 = dot %ta, %tb.T, acc=%acc",
+        f"    %ok1 = add %ok, {BK}",
+        "    yield %acc1, %ok1",
+        "  }",
+        "  store c[%r, %tnr] = %acc",
+        "}",
+    ]) + "\n"
+
+
+def gemm_act_src(M: int, N: int, K: int, BM: int, BN: int, BK: int, elem: str = "int") -> str:
+    """gemm_act.k shape (ref proj/kernels/gemm_act.k:2-18): the stored value is relu of the
+    accumulator after the last iteration (yielded through %last)."""
+    tm = M // BM
+    return "\n".join([
+        f"kernel gemm_act(a: buf<{M}x{K} {elem}>, b: buf<{N}x{K} {elem}>, c: buf<{M}x{N} {elem}>) {{",
+        "  %p = pid",
+        f"  %pm = mod %p, {tm}",
+        f"  %pn = div %p, {tm}",
+        f"  %r = mul %pm, {BM}",
+        f"  %cn = mul %pn, {BN}",
+        f"  %z = const zeros : {BM}x{BN} {elem}",
+        "  %k0 = const 0",
+        f"  loop %k in 0..{K // BK} iter (%acc = %z, %last = %z, %ok = %k0) {{",
+        f"    %ta = tma_load a[%r, %ok] : {BM}x{BK} {elem}",
+        f"    %tb = tma_load b[%cn, %ok] : {BN}x{BK} {elem}",
+        "    %acc1 = dot %ta, %tb.T, acc=%acc",
+        "    %rl = ew relu %acc1",
+        f"    %ok1 = add %ok, {BK}",
+        "    yield %acc1, %rl, %ok1",
+        "  }",
+        "  store c[%r, %cn] = %last",
+        "}",
+    ]) + "\n"

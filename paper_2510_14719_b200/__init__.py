@@ -3,7 +3,7 @@
 The hot path of arxiv 2510.14719 (Tawa) behind the reference's operator interface; see
 DESIGN.md. Public API: gemm_tn, attn_fwd (ops.py), the C-ABI in include/ws.h (libws.so).
 """
-from .ops import attn_fwd, gemm_tn, launch_count  # noqa: F401
+from .ops import attn_fwd, gemm_tn, launch_count, run_kernel  # noqa: F401
 from ._lib import WsError  # noqa: F401
 
-__all__ = ["gemm_tn", "attn_fwd", "launch_count", "WsError"]
+__all__ = ["gemm_tn", "attn_fwd", "run_kernel", "launch_count", "WsError"]

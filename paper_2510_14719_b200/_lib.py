@@ -32,6 +32,7 @@ class GemmDesc(ctypes.Structure):
         ("D", ctypes.c_int32), ("P", ctypes.c_int32),
         ("persistent", ctypes.c_int32), ("cta_pair", ctypes.c_int32),
         ("bn", ctypes.c_int32), ("group_m", ctypes.c_int32),
+        ("act", ctypes.c_int32),
     ]
 
 
@@ -49,11 +50,22 @@ class AttnDesc(ctypes.Structure):
     ]
 
 
+class KBuffer(ctypes.Structure):
+    _fields_ = [
+        ("name", ctypes.c_char_p),
+        ("rows", ctypes.c_int64), ("cols", ctypes.c_int64),
+        ("is_real", ctypes.c_int32),
+        ("data", ctypes.c_void_p),
+    ]
+
+
 # every symbol include/ws.h declares, with its ctypes signature
 EXPORTS = {
     "ws_gemm_tn": (ctypes.c_int, [ctypes.POINTER(GemmDesc), ctypes.c_void_p]),
     "ws_attn_fwd": (ctypes.c_int, [ctypes.POINTER(AttnDesc), ctypes.c_void_p]),
     "ws_attn_fwd_traced": (ctypes.c_int, [ctypes.POINTER(AttnDesc), ctypes.c_void_p, ctypes.c_void_p]),
+    "ws_run_kernel": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(KBuffer), ctypes.c_int32, ctypes.c_int64,
+                                     ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]),
     "ws_last_error": (ctypes.c_char_p, []),
     "ws_launch_count": (ctypes.c_int64, []),
     "ws_version": (ctypes.c_char_p, []),

@@ -32,6 +32,14 @@ ws_status fail(ws_status s, const std::string& msg) {
   return s;
 }
 
+}  // namespace
+
+namespace ws_detail {
+ws_status set_error(ws_status s, const std::string& m) { return fail(s, m); }
+}  // namespace ws_detail
+
+namespace {
+
 #define WS_CUDA_CHECK(expr)                                                                       \
   do {                                                                                            \
     cudaError_t e_ = (expr);                                                                      \
@@ -131,6 +139,7 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   p.group_m = d.group_m > 0 ? d.group_m : 16 / CG;
   if (p.group_m > p.num_m_blocks / CG) p.group_m = p.num_m_blocks / CG;
   p.scale = d.scale_a * d.scale_b;
+  p.act = d.act;
 
   CUtensorMap ta, tb, tc;
   ws_status s;
@@ -271,6 +280,7 @@ ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
   if (d.M <= 0 || d.N <= 0 || d.K <= 0) return fail(WS_TYPE, "M, N, K must be positive");
   if (!d.A || !d.B || !d.C) return fail(WS_TYPE, "null operand pointer");
   if (d.D < 0 || d.P < 0) return fail(WS_PIPELINE_INFEASIBLE, "D and P must be >= 1 (0 = auto)");
+  if (d.act != 0 && d.act != 1) return fail(WS_TYPE, "act must be 0 (none) or 1 (relu)");
   if (d.D > 0 && d.P > d.D)
     return fail(WS_PIPELINE_INFEASIBLE,
                 "MMA pipelining depth P=" + std::to_string(d.P) + " exceeds aref depth D=" + std::to_string(d.D));

@@ -36,6 +36,7 @@ struct GemmParams {
   int mma_depth;  // P
   int group_m;
   float scale;
+  int act;  // 0 none, 1 relu
 };
 
 struct GemmSmemLayout {
@@ -206,6 +207,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     uint8_t* stage_base = smem + L.epi_offset + q * 2 * GEMM_EPI_BUF_BYTES;
     uint32_t acc_stage = 0, acc_phase = 0, chunk_ctr = 0;
     const float scale = p.scale;
+    const float lo_clamp = p.act == 1 ? 0.f : -INFINITY;  // relu epilogue (gemm_act.k)
     for (int t = tile0; t < num_tiles; t += tile_stride) {
       int mb, nb;
       gemm_tile_coords(t, p, p.num_m_blocks / CG, mb, nb);
@@ -245,14 +247,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int j = 0; j < 8; ++j) {
           uint32_t w0, w1, w2, w3;
           if constexpr (OUT == OUT_F32) {
-            w0 = __float_as_uint(__uint_as_float(v[4 * j + 0]) * scale);
-            w1 = __float_as_uint(__uint_as_float(v[4 * j + 1]) * scale);
-            w2 = __float_as_uint(__uint_as_float(v[4 * j + 2]) * scale);
-            w3 = __float_as_uint(__uint_as_float(v[4 * j + 3]) * scale);
+            w0 = __float_as_uint(fmaxf(__uint_as_float(v[4 * j + 0]) * scale, lo_clamp));
+            w1 = __float_as_uint(fmaxf(__uint_as_float(v[4 * j + 1]) * scale, lo_clamp));
+            w2 = __float_as_uint(fmaxf(__uint_as_float(v[4 * j + 2]) * scale, lo_clamp));
+            w3 = __float_as_uint(fmaxf(__uint_as_float(v[4 * j + 3]) * scale, lo_clamp));
           } else {
             float f[8];
 #pragma unroll
-            for (int e = 0; e < 8; ++e) f[e] = __uint_as_float(v[8 * j + e]) * scale;
+            for (int e = 0; e < 8; ++e) f[e] = fmaxf(__uint_as_float(v[8 * j + e]) * scale, lo_clamp);
             if constexpr (OUT == OUT_BF16) {
               w0 = pack_bf16(f[0], f[1]);
               w1 = pack_bf16(f[2], f[3]);

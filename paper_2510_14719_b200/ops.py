@@ -113,5 +113,45 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool 
     return out, lse
 
 
+def run_kernel(text: str, buffers: dict, pid_range=(0, 1), dtype: torch.dtype = torch.bfloat16,
+               stream: Optional[torch.cuda.Stream] = None) -> dict:
+    """Run pids [lo, hi) of a `.k` kernel (reference grammar) on the GPU — the drop-in for the
+    reference's tile-by-tile oracle run `interpret_tiles` (ref proj/tests/support/fixtures.hpp:148-157).
+
+    buffers: {param name: numpy array} (float64 for `real`, int64 for `int` params); arrays are
+    updated in place with the kernel's stores and also returned. Parameters without a buffer start
+    zeroed (and are returned). See ws_run_kernel in include/ws.h for the supported kernel shapes."""
+    import re
+
+    import numpy as np
+
+    # parameters the caller did not pass start zeroed (ref interp.hpp:140-154) and are returned
+    header = text[text.index("(") + 1:text.index(")")]
+    for name, r, c, elem in re.findall(r"(\w+)\s*:\s*buf<(\d+)x(\d+)\s+(int|real)>", header):
+        if name not in buffers:
+            buffers[name] = np.zeros((int(r), int(c)), dtype=np.float64 if elem == "real" else np.int64)
+    keep = []
+    arr = []
+    for name, a in buffers.items():
+        a = np.asarray(a)
+        if a.dtype not in (np.float64, np.int64) or not a.flags.c_contiguous:
+            raise _lib.WsError(2, f"buffer {name!r} must be a C-contiguous float64 or int64 array")
+        b = _lib.KBuffer()
+        nm = name.encode()
+        keep.append(nm)
+        b.name = nm
+        b.rows, b.cols = (a.shape[0], a.shape[1]) if a.ndim == 2 else (a.shape[0], 1)
+        b.is_real = int(a.dtype == np.float64)
+        b.data = a.ctypes.data
+        arr.append(b)
+        buffers[name] = a
+    bufs = (_lib.KBuffer * max(1, len(arr)))(*arr)
+    lo, hi = pid_range
+    lib = _lib.load()
+    _lib.check(lib.ws_run_kernel(text.encode(), bufs, len(arr), lo, hi, _DT[dtype],
+                                 ctypes.c_void_p(_stream_ptr(stream) if torch.cuda.is_available() else 0)))
+    return buffers
+
+
 def launch_count() -> int:
     return int(_lib.load().ws_launch_count())

@@ -28,6 +28,12 @@ CASES = {
                                    K.gemm_tiles(64, 64, 32, 32), {}),
     "gemm_int_32x32x32": (K.gemm_src(32, 32, 32, 8, 8, 8, elem="int"), 2026, 16, {}),
     "gemm_int_seed7_16x16x24": (K.gemm_src(16, 16, 24, 8, 8, 8, elem="int"), 7, 4, {}),
+    # the other gemm.k-family forms (shapes of ref proj/kernels/gemm_batched.k, gemm_act.k,
+    # gemm_large.k), integer payloads like the shipped files
+    "gemm_batched_int_4x16x16": (K.gemm_batched_src(4, 16, 8, 16, 8), 2026, 16, {}),
+    "gemm_act_int_32x32x32": (K.gemm_act_src(32, 32, 32, 8, 8, 8), 2026, 16, {}),
+    "gemm_large_int_32x32x32": (K.gemm_src(32, 32, 32, 16, 16, 16, elem="int"), 2026, 4, {}),
+    "gemm_act_real_64x64x64": (K.gemm_act_src(64, 64, 64, 32, 32, 16, elem="real"), 2026, 4, {}),
     "flash_bh3_s64_d16": (K.flash_src(3, 64, 16, 16, causal=False), 2026, 3 * 4, {"mb": K.flash_mask_bank(16)}),
     "flash_causal_bh3_s64_d16": (K.flash_src(3, 64, 16, 16, causal=True), 2026, 3 * 4,
                                  {"mb": K.flash_mask_bank(16)}),

@@ -18,7 +18,7 @@ def _declared_functions():
 
 def test_header_declares_the_path():
     assert _declared_functions() == ["ws_attn_fwd", "ws_attn_fwd_traced", "ws_gemm_tn", "ws_last_error",
-                                    "ws_launch_count", "ws_version"]
+                                    "ws_launch_count", "ws_run_kernel", "ws_version"]
 
 
 def test_library_exports_every_declared_symbol(ws):
@@ -33,8 +33,8 @@ def test_library_exports_every_declared_symbol(ws):
 def test_desc_layout_matches_header():
     from paper_2510_14719_b200 import _lib
 
-    # in_dtype,out_dtype (8) + M,N,K (24) + A,lda,B,ldb,C,ldc (48) + scales (8) + 6 ints (24)
-    assert ctypes.sizeof(_lib.GemmDesc) == 112
+    # in_dtype,out_dtype (8) + M,N,K (24) + A,lda,B,ldb,C,ldc (48) + scales (8) + 7 ints (28) -> 116, padded 120
+    assert ctypes.sizeof(_lib.GemmDesc) == 120
     assert ctypes.sizeof(_lib.AttnDesc) == 4 * 7 + 4 + 8 * 5 + 4 * 3 + 4  # padded to 8
 
 
@@ -61,6 +61,7 @@ def _gemm_desc(ws, **kw):
     (dict(in_dtype=0), "type"),                     # fp32 inputs are not a tensor-core kind here
     (dict(bn=96), "type"),
     (dict(lda=128), "type"),
+    (dict(act=2), "type"),
 ])
 def test_gemm_validation_codes(ws, kw, code):
     lib = ws._lib.load()
