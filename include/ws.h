@@ -98,6 +98,9 @@ typedef struct ws_attn_desc {
   float* LSE;
   int32_t D;                   /* K/V aref depth; 0 = auto */
   int32_t bh_begin, bh_end;
+  int32_t kv_block;            /* keys per K/V block: 0 = auto (128), 64 or 128. 128-key blocks
+                                  keep the QK^T MMA inside the shared-memory operand rate; 64
+                                  double-buffers S per Q tile instead (csrc/attn*_sm100.cuh) */
 } ws_attn_desc;
 
 ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream);

@@ -47,6 +47,7 @@ class AttnDesc(ctypes.Structure):
         ("LSE", ctypes.c_void_p),
         ("D", ctypes.c_int32),
         ("bh_begin", ctypes.c_int32), ("bh_end", ctypes.c_int32),
+        ("kv_block", ctypes.c_int32),
     ]
 
 

@@ -19,6 +19,7 @@
 #include <string>
 
 #include "../../include/ws.h"
+#include "attn128_sm100.cuh"
 #include "attn_sm100.cuh"
 #include "gemm_sm100.cuh"
 
@@ -246,6 +247,50 @@ ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stre
   return WS_OK;
 }
 
+template <int DH, bool BF16>
+ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stream, unsigned long long* trace) {
+  using namespace ws;
+  const int dt = d.dtype;
+  const int64_t rows = (int64_t)d.B * d.H * d.S;
+  Attn128Params p;
+  p.S = d.S;
+  p.BH_begin = bh0;
+  p.num_pairs = d.S / (2 * A128_BM);
+  p.causal = d.causal;
+  // causal: (b,h) fastest so every head's heaviest query pairs run first (longest-first);
+  // non-causal: the query pairs of one (b,h) run together and share its K/V in L2
+  p.bh_fast = d.causal ? 1 : 0;
+  const float sm = d.softmax_scale > 0.f ? d.softmax_scale : 1.0f / std::sqrt((float)DH);
+  p.scale_log2 = sm * 1.4426950408889634f;
+  p.lse = d.LSE;
+  p.o = d.O;
+  p.trace = trace;
+  int max_stages = (SMEM_LIMIT - (int)a128_smem_bytes(DH, 0)) / (int)a128_kv_bytes(DH);
+  if (max_stages > A128_MAX_STAGES) max_stages = A128_MAX_STAGES;
+  p.kv_stages = d.D > 0 ? d.D : max_stages;
+  if (p.kv_stages < 2)
+    return fail(WS_PIPELINE_INFEASIBLE, "the K/V aref needs D >= 2 (ref pipeline.hpp:309-315)");
+  const uint32_t smem = a128_smem_bytes(DH, p.kv_stages);
+  if (p.kv_stages > A128_MAX_STAGES || (int)smem > SMEM_LIMIT)
+    return fail(WS_SMEM_OVERFLOW, "D=" + std::to_string(p.kv_stages) + " K/V stages need " + std::to_string(smem) +
+                                      " B of shared memory; limit " + std::to_string(SMEM_LIMIT));
+  CUtensorMap tq, tk, tv;
+  ws_status s;
+  if ((s = make_tmap(&tq, d.Q, dt, rows, DH, DH, A128_BM, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
+  if ((s = make_tmap(&tk, d.K, dt, rows, DH, DH, A128_BN, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
+  if ((s = make_tmap(&tv, d.V, dt, rows, DH, DH, A128_BN, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
+  auto kern = ws_attn128_kernel<DH, BF16>;
+  WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = p.bh_fast ? dim3(bh1 - bh0, p.num_pairs) : dim3(p.num_pairs, bh1 - bh0);
+  cfg.blockDim = dim3(A128_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, p));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return WS_OK;
+}
+
 ws_status attn_entry(const ws_attn_desc& d, cudaStream_t st, unsigned long long* trace) {
   if (d.dtype != WS_BF16 && d.dtype != WS_F16) return fail(WS_TYPE, "attention dtype must be BF16 or F16");
   if (d.B <= 0 || d.H <= 0 || d.S <= 0) return fail(WS_TYPE, "B, H, S must be positive");
@@ -258,6 +303,15 @@ ws_status attn_entry(const ws_attn_desc& d, cudaStream_t st, unsigned long long*
   const int bh0 = d.bh_begin, bh1 = d.bh_end > 0 ? d.bh_end : BH;
   if (bh0 < 0 || bh1 > BH || bh0 >= bh1) return fail(WS_TYPE, "bad (b,h) shard range");
   if ((int64_t)BH * d.S >= (int64_t)1 << 31) return fail(WS_TYPE, "B*H*S must fit in int32");
+  if (d.kv_block != 0 && d.kv_block != 64 && d.kv_block != 128)
+    return fail(WS_TYPE, "kv_block must be 0 (auto), 64 or 128");
+  if (d.kv_block != 64) {
+    if (d.Dh == 128)
+      return d.dtype == WS_BF16 ? launch_attn128<128, true>(d, bh0, bh1, st, trace)
+                                : launch_attn128<128, false>(d, bh0, bh1, st, trace);
+    return d.dtype == WS_BF16 ? launch_attn128<64, true>(d, bh0, bh1, st, trace)
+                              : launch_attn128<64, false>(d, bh0, bh1, st, trace);
+  }
   if (d.Dh == 128)
     return d.dtype == WS_BF16 ? launch_attn<128, true>(d, bh0, bh1, st, trace)
                               : launch_attn<128, false>(d, bh0, bh1, st, trace);

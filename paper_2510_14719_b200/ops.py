@@ -76,12 +76,13 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
 def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool = False,
              softmax_scale: Optional[float] = None, out: Optional[torch.Tensor] = None,
              lse: Optional[torch.Tensor] = None, D: int = 0, bh_range: Optional[tuple] = None,
-             stream: Optional[torch.cuda.Stream] = None, trace: Optional[torch.Tensor] = None):
+             stream: Optional[torch.cuda.Stream] = None, trace: Optional[torch.Tensor] = None,
+             kv_block: int = 0):
     """FlashAttention forward over [B, H, S, Dh] tensors. Returns (o, lse) with lse fp32 [B, H, S]
     in natural-log units (lse = m + log l of the .k's running max m and row sum l).
 
     trace: optional int64 CUDA tensor of 3*256*8 entries receiving %clock64 stamps of CTA (0,0)
-    (see ws_attn_fwd_traced in include/ws.h)."""
+    (see ws_attn_fwd_traced in include/ws.h). kv_block: keys per K/V block (0 = auto = 128, or 64)."""
     if q.device.type != "cuda":
         raise _lib.WsError(2, "operands must be CUDA tensors (no CPU path)")
     if not (q.dtype == k.dtype == v.dtype) or q.dtype not in (torch.float16, torch.bfloat16):
@@ -104,6 +105,7 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool 
     d.D = D
     lo, hi = bh_range if bh_range is not None else (0, B * H)
     d.bh_begin, d.bh_end = lo, hi
+    d.kv_block = kv_block
     lib = _lib.load()
     if trace is not None:
         _lib.check(lib.ws_attn_fwd_traced(ctypes.byref(d), ctypes.c_void_p(_stream_ptr(stream)),

@@ -27,35 +27,39 @@ def check(B, H, S, Dh, causal, dt=torch.bfloat16, scale_in=1.0, **kw):
     le = (lse.double() - rl).abs().max().item()
     print(f"B={B} H={H} S={S} Dh={Dh} causal={causal} {dt} {kw}: O relerr={rel:.3e} lse abserr={le:.3e} nan={torch.isnan(o).any().item()}", flush=True)
 
-def bench(B, H, S, Dh, causal, iters=10, dt=torch.bfloat16):
+def bench(B, H, S, Dh, causal, iters=10, dt=torch.bfloat16, **kw):
     q = torch.randn(B, H, S, Dh, device="cuda", dtype=dt); k = torch.randn_like(q); v = torch.randn_like(q)
     o = torch.empty_like(q); lse = torch.empty(B, H, S, device="cuda")
-    for _ in range(3): ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse)
+    for _ in range(3): ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse, **kw)
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
     e0.record()
-    for _ in range(iters): ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse)
+    for _ in range(iters): ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse, **kw)
     e1.record(); torch.cuda.synchronize()
     ms = e0.elapsed_time(e1) / iters
     fl = 4 * B * H * S * S * Dh / (2 if causal else 1)
-    print(f"BENCH attn B={B} H={H} S={S} Dh={Dh} causal={causal}: {ms:.3f} ms {fl/ms/1e9:.1f} TFLOP/s", flush=True)
+    print(f"BENCH attn B={B} H={H} S={S} Dh={Dh} causal={causal} {kw}: {ms:.3f} ms {fl/ms/1e9:.1f} TFLOP/s", flush=True)
 
 if __name__ == "__main__":
     torch.cuda.init()
-    check(1, 1, 256, 128, False)
-    check(1, 2, 512, 128, False)
-    check(1, 2, 512, 64, False)
-    check(1, 2, 512, 128, True)
-    check(1, 2, 512, 64, True)
-    check(2, 3, 1024, 128, False, dt=torch.float16)
-    check(1, 2, 1024, 128, True, scale_in=0.25)
-    for D in (2, 3, 4, 5):
-        check(1, 2, 1024, 128, True, D=D)
-        check(1, 2, 1024, 64, False, D=D)
-    for S in (1024, 4096, 16384):
-        bench(16384 // S, 16, S, 128, False)
-    bench(1, 16, 16384, 128, True)
-    bench(1, 16, 16384, 64, True)
+    kvb = [int(x) for x in os.environ.get("KVB", "128,64").split(",")]
+    for kb in kvb:
+        check(1, 1, 256, 128, False, kv_block=kb)
+        check(1, 2, 512, 128, False, kv_block=kb)
+        check(1, 2, 512, 64, False, kv_block=kb)
+        check(1, 2, 512, 128, True, kv_block=kb)
+        check(1, 2, 512, 64, True, kv_block=kb)
+        check(2, 3, 1024, 128, False, dt=torch.float16, kv_block=kb)
+        check(1, 2, 1024, 128, True, scale_in=0.25, kv_block=kb)
+        for D in (2, 3, 4, 5):
+            check(1, 2, 1024, 128, True, D=D, kv_block=kb)
+            check(1, 2, 1024, 64, False, D=D, kv_block=kb)
+    for kb in kvb:
+        for S in (1024, 4096, 16384):
+            bench(16384 // S, 16, S, 128, False, kv_block=kb)
+        bench(1, 16, 16384, 128, True, kv_block=kb)
+        bench(1, 16, 16384, 64, True, kv_block=kb)
+        bench(1, 16, 16384, 64, False, kv_block=kb)
     try:
         from flash_attn import flash_attn_func
         q = torch.randn(1, 16384, 16, 128, device="cuda", dtype=torch.bfloat16); k = torch.randn_like(q); v = torch.randn_like(q)
