@@ -1,92 +1,67 @@
-// attn128_sm100.cuh — FlashAttention forward for sm_100a with 128-key K/V blocks.
+// attn_psmem_sm100.cuh — FlashAttention forward for sm_100a, 128-key K/V blocks, P staged in
+// shared memory.
 //
-// Same reference semantics as attn_sm100.cuh (the flash .k of SURVEY.md Appendix A: the coarse
-// T/C/U pipeline of ref proj/include/warpspec/pipeline.hpp:160-328, schedule.hpp:18-74), with a
-// different mapping onto the SM:
+// Same reference semantics as attn_sm100.cuh / attn128_sm100.cuh (the flash .k of SURVEY.md
+// Appendix A: coarse T/C/U pipeline, ref proj/include/warpspec/pipeline.hpp:160-328,
+// schedule.hpp:18-74). What changes is where P lives:
 //
-//   * K/V blocks of 128 keys. A 128x128xDh QK^T MMA reads 4 KB of Q and 4 KB of K from shared
-//     memory per K=16 step and runs 64 cycles — inside the 128 B/clk shared-memory operand rate.
-//     The 64-key kernel's QK (4 KB + 2 KB per 32-cycle step) is bound by that rate at 1.5x its
-//     tensor time, which is the loss this variant removes.
-//   * TMEM (512 columns for Dh = 128): S_0 | S_1 (128 columns each) | O_0 | O_1 (Dh each). The S
-//     accumulator of a Q tile is single-buffered; the overlap the coarse schedule asks for (T_{j+1}
-//     while C_j runs) comes from the two Q tiles (the cooperative row bands of
-//     ref proj/include/warpspec/grid.hpp:24-72) ping-ponging on the tensor core: while the softmax
-//     warps of tile 0 work on S_0(j), the tensor core runs PV_1(j-1) and QK_1(j) for tile 1.
-//   * Issue order of the single MMA thread, per step j:
-//         PV_0(j)  QK_0(j+1)  PV_1(j)  QK_1(j+1)
-//     QK_t(j+1) overwrites S_t, whose first 64 columns hold P_t(j) read by PV_t(j); tcgen05 MMAs
-//     of one thread execute in issue order, so the overwrite follows the read. A commit after
-//     QK_t(j+1) therefore also proves PV_t(j) complete: when the softmax warps see S_t(j+1) they
-//     may rescale O_t in place (the correction stage needs no separate barrier).
-//   * Causal: the 256 query rows of a CTA are two 128-row tiles aligned to 128-key blocks, so the
-//     diagonal block of each tile is square and is the only block that needs a mask; tile 0 stops
-//     one block before tile 1.
+//   attn128: P_t(j) is written back over S_t in TMEM, so QK_t(j+1) can only be issued after
+//            PV_t(j) — the T stage of block j+1 waits for the whole C stage of block j, and the
+//            tile's chain per block is softmax + PV + QK (measured ~3000 cycles per 128 keys).
+//   here:    the softmax warps copy S_t(j) into registers and release it at once (s_free), and
+//            P_t(j) goes to a shared-memory tile read by an SS-form PV MMA (128x128x16 SS MMAs run
+//            at the tensor floor, scripts/micro/mma_rate.cu). QK_t(j+1) therefore runs while the
+//            softmax of block j is still exponentiating — the coarse schedule's "T_{j+1} overlaps
+//            C_j" (ref schedule.hpp:18-74) for both Q tiles at once, with S single-buffered in TMEM.
+//
+// TMEM (512 columns): S_0 | S_1 (128 each) | O_0 | O_1 (Dh each).
+// Shared memory: Q_0 | Q_1 | P_0 | P_1 (128 x 128 bf16, K-major SW128, the A operand of PV) | K/V ring.
+// Barriers per Q tile t (each completes once per block, and no party can run a phase ahead of a
+// waiter that has not yet seen the previous phase, so parity tests never alias):
+//   s_full[t]  QK_t(j) complete                          (tcgen05.commit)
+//   s_free[t]  S_t(j) copied to registers                 (4 softmax warps)
+//   p_full[t]  P_t(j) in shared memory, O_t rescaled      (4 softmax warps)
+//   pv_done[t] PV_t(j) complete: P_t and O_t reusable     (tcgen05.commit)
 #pragma once
 
-#include "attn_sm100.cuh"  // ATTN_RESCALE_THRESHOLD, attn_poly_pair, trace layout
+#include "attn128_sm100.cuh"
 
 namespace ws {
 
-constexpr int A128_BM = 128;          // query rows per Q tile (one TMEM lane each)
-constexpr int A128_BN = 128;          // keys per K/V block
-constexpr int A128_THREADS = 384;     // 8 softmax warps + producer + MMA + TMEM allocator + spare
-constexpr int A128_MAX_STAGES = 8;
-constexpr int A128_POLY = 2;          // default exp mix: 2 of every 8 column pairs on the FMA pipe
-
-struct Attn128Params {
-  int S, BH_begin, num_pairs;  // num_pairs = S / 256 work items per (b,h)
-  int kv_stages;
-  int causal;
-  int bh_fast;        // grid order: 1 = blockIdx.x walks (b,h) (causal, heaviest pairs first);
-                      // 0 = blockIdx.x walks the query pairs of one (b,h) (K/V stay L2-resident)
-  float scale_log2;   // softmax_scale * log2(e)
-  float* lse;
-  void* o;
-  unsigned long long* trace;  // optional %clock64 stamps of CTA (0,0), layout of attn_sm100.cuh
-};
-
-__host__ __device__ inline uint32_t a128_q_bytes(int Dh) { return A128_BM * Dh * 2; }
-__host__ __device__ inline uint32_t a128_kv_bytes(int Dh) { return A128_BN * Dh * 2; }
-__host__ __device__ inline uint32_t a128_smem_bytes(int Dh, int kv_stages) {
-  // Q0 | Q1 | kv slots | barriers (+1 KB alignment slack)
-  return 2 * a128_q_bytes(Dh) + kv_stages * a128_kv_bytes(Dh) + (2 * A128_MAX_STAGES + 16) * 8 + 16 + 1024;
+__host__ __device__ inline uint32_t aps_smem_bytes(int Dh, int kv_stages) {
+  // Q0 | Q1 | P0 | P1 | kv slots | barriers (+1 KB alignment slack)
+  return 2 * a128_q_bytes(Dh) + 2 * A128_BM * A128_BN * 2 + kv_stages * a128_kv_bytes(Dh) +
+         (2 * A128_MAX_STAGES + 16) * 8 + 16 + 1024;
 }
 
-__device__ __forceinline__ float fmax3(float a, float b, float c) {
-  float d;
-  asm("max.f32 %0, %1, %2, %3;" : "=f"(d) : "f"(a), "f"(b), "f"(c));
-  return d;
-}
-
-// POLY: how many of every 8 column pairs are exponentiated on the FMA pipe (exp2_poly2) instead of
-// MUFU.EX2 — see attn_poly_pair in attn_sm100.cuh.
 template <int DH, bool BF16, int POLY = 2, bool TRACE = false>
 __global__ void __launch_bounds__(A128_THREADS, 1)
-    ws_attn128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                      const __grid_constant__ CUtensorMap tm_v, const Attn128Params p) {
-  constexpr uint32_t QTILE = A128_BM * DH * 2;   // bytes of a 128 x DH Q tile
-  constexpr uint32_t KVTILE = A128_BN * DH * 2;  // bytes of a 128 x DH K or V block
-  constexpr uint32_t QPANEL = A128_BM * 128;     // one 64-column (128 B) swizzle panel of Q
-  constexpr uint32_t KVPANEL = A128_BN * 128;    // one 64-column panel of K / V
+    ws_attn_psmem_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
+                         const __grid_constant__ CUtensorMap tm_v, const Attn128Params p) {
+  constexpr uint32_t QTILE = A128_BM * DH * 2;       // bytes of a 128 x DH Q tile
+  constexpr uint32_t PTILE = A128_BM * A128_BN * 2;  // bytes of a 128 x 128 P tile
+  constexpr uint32_t KVTILE = A128_BN * DH * 2;      // bytes of a 128 x DH K or V block
+  constexpr uint32_t PANEL = 128 * 128;              // one 64-column (128 B) swizzle panel of 128 rows
   constexpr int NPANEL = DH / 64;
   constexpr uint32_t FMT = BF16 ? 1u : 0u;
   constexpr uint32_t IDESC_QK = make_idesc(FMT, A128_BM, A128_BN, 0, 0);
-  constexpr uint32_t IDESC_PV = make_idesc(FMT, A128_BM, DH, 0, 1);  // B = V is MN-major
+  constexpr uint32_t IDESC_PV = make_idesc(FMT, A128_BM, DH, 0, 1);  // A = P K-major, B = V MN-major
   constexpr uint32_t COL_O = 2 * A128_BN;
   constexpr uint32_t TMEM_COLS = 2 * A128_BN + 2 * DH <= 256 ? 256 : 512;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  uint8_t* sq = smem;               // Q0, Q1
-  uint8_t* skv = smem + 2 * QTILE;  // K/V ring
+  uint8_t* sq = smem;                  // Q0, Q1
+  uint8_t* sp = smem + 2 * QTILE;      // P0, P1
+  uint8_t* skv = sp + 2 * PTILE;       // K/V ring
   uint8_t* bar_base = skv + p.kv_stages * KVTILE;
   auto* ring = reinterpret_cast<ArefBarriers<A128_MAX_STAGES>*>(bar_base);
   uint64_t* q_full = reinterpret_cast<uint64_t*>(bar_base + 2 * A128_MAX_STAGES * 8);
-  uint64_t* s_full = q_full + 1;  // [2]: QK_t(j) complete (and with it PV_t(j-1))
-  uint64_t* p_full = q_full + 3;  // [2]: P_t(j) in S_t, O_t rescaled
-  uint64_t* o_full = q_full + 5;  // [2]: last PV_t complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 7);
+  uint64_t* s_full = q_full + 1;   // [2]
+  uint64_t* s_free = q_full + 3;   // [2]
+  uint64_t* p_full = q_full + 5;   // [2]
+  uint64_t* pv_done = q_full + 7;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 9);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -104,7 +79,6 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
   // K/V blocks per tile: causal tile t of pair i sees blocks 0 .. 2i+t (its diagonal block last)
   const int n0 = p.causal ? 2 * pair + 1 : p.S / A128_BN;
   const int n1 = p.causal ? 2 * pair + 2 : p.S / A128_BN;
-  // the traced instantiation (ws_attn_fwd_traced) is the only one carrying the stamps
   unsigned long long* const trace =
       (TRACE && p.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) ? p.trace : nullptr;
 #define WS_TRACE(role, j, ev)                                                        \
@@ -121,8 +95,9 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     mbar_init(q_full, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
+      mbar_init(&s_free[i], 4);
       mbar_init(&p_full[i], 4);
-      mbar_init(&o_full[i], 1);
+      mbar_init(&pv_done[i], 1);
     }
     fence_barrier_init();
   } else if (warp == 10) {
@@ -144,7 +119,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       for (int t = 0; t < 2; ++t)
 #pragma unroll
         for (int h = 0; h < NPANEL; ++h)
-          tma_load_2d(sq + t * QTILE + h * QPANEL, &tm_q, q_full, h * 64, q_row0 + t * A128_BM);
+          tma_load_2d(sq + t * QTILE + h * PANEL, &tm_q, q_full, h * 64, q_row0 + t * A128_BM);
       ArefCursor c;
       const int kv_row0 = bh * p.S;
       auto put = [&](const CUtensorMap* m, int blk) {
@@ -153,7 +128,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         uint8_t* dst = skv + c.slot * KVTILE;
 #pragma unroll
         for (int h = 0; h < NPANEL; ++h)
-          tma_load_2d(dst + h * KVPANEL, m, &ring->full[c.slot], h * 64, kv_row0 + blk * A128_BN);
+          tma_load_2d(dst + h * PANEL, m, &ring->full[c.slot], h * 64, kv_row0 + blk * A128_BN);
         c.advance(D);
       };
       put(&tm_k, 0);
@@ -166,23 +141,24 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     // ===================== MMA issuer (whole warp, one elected lane issues) =====================
     regs_dec<72>();
     const uint64_t qdesc = make_sw128_desc(smem_u32(sq), 16, 1024);
+    const uint64_t pdesc = make_sw128_desc(smem_u32(sp), 16, 1024);
     const uint64_t kdesc = make_sw128_desc(smem_u32(skv), 16, 1024);
-    const uint64_t vdesc = make_sw128_desc(smem_u32(skv), KVPANEL, 1024);
+    const uint64_t vdesc = make_sw128_desc(smem_u32(skv), PANEL, 1024);
     auto issue_qk = [&](int t, uint32_t k_slot) {
       const uint64_t a0 = qdesc + ((t * QTILE) >> 4), b0 = kdesc + ((k_slot * KVTILE) >> 4);
 #pragma unroll
       for (int k = 0; k < DH / 16; ++k) {
-        const uint32_t off = ((k / 4) * KVPANEL + (k % 4) * 32) >> 4;
-        const uint32_t qoff = ((k / 4) * QPANEL + (k % 4) * 32) >> 4;
-        mma_f16_ss_warp(tmem + t * A128_BN, a0 + qoff, b0 + off, IDESC_QK, k != 0);
+        const uint32_t off = ((k / 4) * PANEL + (k % 4) * 32) >> 4;
+        mma_f16_ss_warp(tmem + t * A128_BN, a0 + off, b0 + off, IDESC_QK, k != 0);
       }
     };
     auto issue_pv = [&](int t, uint32_t v_slot, bool acc) {
-      const uint64_t b0 = vdesc + ((v_slot * KVTILE) >> 4);
+      const uint64_t a0 = pdesc + ((t * PTILE) >> 4), b0 = vdesc + ((v_slot * KVTILE) >> 4);
 #pragma unroll
       for (int k = 0; k < A128_BN / 16; ++k) {
-        // A = P_t: 16 keys = 8 packed columns; B = V rows [16k, 16k+16) (two 8-row core groups)
-        mma_f16_ts_warp(tmem + COL_O + t * DH, tmem + t * A128_BN + k * 8, b0 + ((k * 16 * 128) >> 4), IDESC_PV,
+        // A = P_t keys [16k, 16k+16) (K-major panel k/4); B = V rows [16k, 16k+16) (two 8-row groups)
+        const uint32_t aoff = ((k / 4) * PANEL + (k % 4) * 32) >> 4;
+        mma_f16_ss_warp(tmem + COL_O + t * DH, a0 + aoff, b0 + ((k * 16 * 128) >> 4), IDESC_PV,
                         (acc || k != 0) ? 1u : 0u);
       }
     };
@@ -198,43 +174,40 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     c.advance(D);
     for (int j = 0; j < n1; ++j) {
       if (lane == 0) WS_TRACE(0, j, 0);
-      const bool more1 = j + 1 < n1;
-      uint32_t kslot = 0;
-      if (more1) {
+      if (j + 1 < n1) {
         ring->get(c, 13);  // K_{j+1}
-        kslot = c.slot;
+        const uint32_t kslot = c.slot;
         c.advance(D);
+        if (j + 1 < n0) {
+          mbar_wait(&s_free[0], j & 1, 17);  // S_0(j) copied out
+          tc_fence_after();
+          issue_qk(0, kslot);
+          mma_commit_warp(&s_full[0]);
+        }
+        if (lane == 0) WS_TRACE(0, j, 1);
+        mbar_wait(&s_free[1], j & 1, 18);
+        tc_fence_after();
+        issue_qk(1, kslot);
+        mma_commit_warp(&s_full[1]);
+        mma_commit_warp(&ring->empty[kslot]);
       }
+      if (lane == 0) WS_TRACE(0, j, 2);
       ring->get(c, 14);  // V_j
       const uint32_t vslot = c.slot;
       c.advance(D);
-      tc_fence_after();
-      if (lane == 0) WS_TRACE(0, j, 1);
       if (j < n0) {
-        mbar_wait(&p_full[0], j & 1, 15);  // C_0(j): P_0(j) in TMEM, O_0 rescaled
+        mbar_wait(&p_full[0], j & 1, 15);  // C_0(j): P_0(j) in smem, O_0 rescaled
         tc_fence_after();
-        if (lane == 0) WS_TRACE(0, j, 2);
-        issue_pv(0, vslot, j > 0);
-        if (j + 1 < n0) {
-          issue_qk(0, kslot);
-          mma_commit_warp(&s_full[0]);
-        } else {
-          mma_commit_warp(&o_full[0]);
-        }
         if (lane == 0) WS_TRACE(0, j, 3);
+        issue_pv(0, vslot, j > 0);
+        mma_commit_warp(&pv_done[0]);
       }
       mbar_wait(&p_full[1], j & 1, 16);
       tc_fence_after();
       if (lane == 0) WS_TRACE(0, j, 4);
       issue_pv(1, vslot, j > 0);
+      mma_commit_warp(&pv_done[1]);
       mma_commit_warp(&ring->empty[vslot]);
-      if (more1) {
-        issue_qk(1, kslot);
-        mma_commit_warp(&s_full[1]);
-        mma_commit_warp(&ring->empty[kslot]);
-      } else {
-        mma_commit_warp(&o_full[1]);
-      }
       if (lane == 0) WS_TRACE(0, j, 5);
     }
   } else if (warp >= 8) {
@@ -242,12 +215,15 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
   } else {
     // ===================== softmax / correction / epilogue =====================
     regs_inc<216>();
-    const int t = warp / 4;        // Q tile
-    const uint32_t q = warp & 3u;  // TMEM lane quarter
+    const int t = warp / 4;         // Q tile
+    const uint32_t q = warp & 3u;   // TMEM lane quarter
     const int row = q * 32 + lane;  // row within the Q tile
     const uint32_t t_lane = (q * 32u) << 16;
     const uint32_t t_s = tmem + t_lane + t * A128_BN;
     const uint32_t t_o = tmem + t_lane + COL_O + t * DH;
+    // this thread's row of P_t: two 128-byte-swizzled panels (keys 0-63, 64-127)
+    const uint32_t p_row = smem_u32(sp + t * PTILE) + row * 128u;
+    const uint32_t swz = static_cast<uint32_t>(row & 7);
     const int n_t = t == 0 ? n0 : n1;
     const int j_diag = p.causal ? n_t - 1 : -1;
     const float sl2 = p.scale_log2;
@@ -266,6 +242,10 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         for (int c0 = 0; c0 < A128_BN; c0 += 32) tmem_ld32(t_s + c0, *reinterpret_cast<uint32_t(*)[32]>(su + c0));
         tmem_wait_ld();
       }
+      // S_t(j) is in registers: release the TMEM columns so QK_t(j+1) can run during this softmax
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&s_free[t]);
       if (tr) WS_TRACE(1 + t, j, 2);
       if (j == j_diag) {
 #pragma unroll
@@ -294,8 +274,10 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         m_used = m_blk;
       }
       if (j > 0 && __any_sync(0xffffffffu, need)) {
-        // correction: S_t(j) complete implies PV_t(j-1) complete (issued before QK_t(j)), and
-        // PV_t(j) waits for this warp's p_full arrival — O_t is quiescent here.
+        // correction: O_t *= alpha once PV_t(j-1) has landed. PV_t(j) needs this warp's p_full,
+        // so pv_done is at most one phase behind and the parity test is unambiguous.
+        mbar_wait(&pv_done[t], (j - 1) & 1, 24 + t);
+        tc_fence_after();
         const uint64_t al2 = f2_pack(alpha, alpha);
 #pragma unroll 1
         for (int c0 = 0; c0 < DH; c0 += 32) {
@@ -311,17 +293,23 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
           }
           tmem_st32(t_o + c0, ov);
         }
+        tmem_wait_st();
       }
       l *= alpha;
       if (tr) WS_TRACE(1 + t, j, 3);
-      // P = 2^(s*sl2 - m) written back over the first 64 columns of S_t as packed 16-bit pairs
+      // P_t's shared-memory tile is free once PV_t(j-1) has read it (long done by now: PV_t(j-1) was
+      // issued when this warp finished block j-1)
+      if (j > 0) mbar_wait(&pv_done[t], (j - 1) & 1, 24 + t);
+      // P = 2^(s*sl2 - m), packed to 16-bit pairs and stored 8 keys (16 bytes) at a time into the
+      // 128B-swizzled K-major P tile as it is produced, so the shared-memory writes overlap the math
       const uint64_t sl2x2 = f2_pack(sl2, sl2), negm2 = f2_pack(-m_used, -m_used);
-      uint64_t sum2a = f2_pack(0.f, 0.f), sum2b = f2_pack(0.f, 0.f);
+      uint64_t sum4[4] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
 #pragma unroll
-      for (int c0 = 0; c0 < A128_BN; c0 += 32) {
-        uint32_t pk[16];
+      for (int ch = 0; ch < A128_BN / 8; ++ch) {
+        uint32_t pk[4];
 #pragma unroll
-        for (int c = c0; c < c0 + 32; c += 2) {
+        for (int e = 0; e < 4; ++e) {
+          const int c = ch * 8 + 2 * e;
           const uint64_t x2 = f2_fma(f2_pack(s[c], s[c + 1]), sl2x2, negm2);
           uint64_t p2;
           if (attn_poly_pair(POLY, (c / 2) & 7)) {
@@ -331,31 +319,30 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
             f2_unpack(x2, x0, x1);
             p2 = f2_pack(ex2_approx(x0), ex2_approx(x1));
           }
-          if ((c / 2) & 1)
-            sum2b = f2_add(sum2b, p2);
-          else
-            sum2a = f2_add(sum2a, p2);
+          sum4[e] = f2_add(sum4[e], p2);
           float p0, p1;
           f2_unpack(p2, p0, p1);
-          pk[(c - c0) / 2] = BF16 ? pack_bf16(p0, p1) : pack_f16(p0, p1);
+          pk[e] = BF16 ? pack_bf16(p0, p1) : pack_f16(p0, p1);
         }
-        tmem_st16(t_s + c0 / 2, pk);
+        // 16-byte chunk ch = keys [8ch, 8ch+8): panel ch/8, swizzled position (ch%8) ^ (row%8)
+        const uint32_t addr = p_row + (ch / 8) * PANEL + ((static_cast<uint32_t>(ch & 7) ^ swz) << 4);
+        st_shared_v4(addr, pk[0], pk[1], pk[2], pk[3]);
       }
       {
         float a, b, c2, d2;
-        f2_unpack(sum2a, a, b);
-        f2_unpack(sum2b, c2, d2);
+        f2_unpack(f2_add(sum4[0], sum4[1]), a, b);
+        f2_unpack(f2_add(sum4[2], sum4[3]), c2, d2);
         l += (a + b) + (c2 + d2);
       }
-      tmem_wait_st();
       if (tr) WS_TRACE(1 + t, j, 4);
+      fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core's reads
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);
       if (tr) WS_TRACE(1 + t, j, 5);
     }
-    // epilogue: O_t / l -> global, lse
-    mbar_wait(&o_full[t], 0, 26 + t);
+    // epilogue: O_t / l -> global, lse once the last PV_t has completed
+    mbar_wait(&pv_done[t], (n_t - 1) & 1, 26 + t);
     tc_fence_after();
     const float inv_l = 1.f / l;
     const size_t grow = static_cast<size_t>(q_row0 + t * A128_BM + row);

@@ -82,6 +82,7 @@ __host__ __device__ inline uint32_t attn_smem_bytes(int Dh, int kv_stages) {
 // MUFU (16 ex2/clk/SM). Measured (scripts/micro/softmax_loop.cu): 3 of 8 is the fastest mix.
 __host__ __device__ constexpr bool attn_poly_pair(int POLY, int i) {
   return POLY == 0 ? false
+       : POLY == 1 ? (i == 3)
        : POLY == 2 ? (i == 1 || i == 5)
        : POLY == 3 ? (i == 1 || i == 4 || i == 6)
        : POLY == 4 ? (i & 1) == 1

@@ -14,12 +14,14 @@
 #include <atomic>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
 
 #include "../../include/ws.h"
 #include "attn128_sm100.cuh"
+#include "attn_psmem_sm100.cuh"
 #include "attn_sm100.cuh"
 #include "gemm_sm100.cuh"
 
@@ -247,7 +249,7 @@ ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stre
   return WS_OK;
 }
 
-template <int DH, bool BF16>
+template <int DH, bool BF16, bool PSMEM>
 ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stream, unsigned long long* trace) {
   using namespace ws;
   const int dt = d.dtype;
@@ -265,12 +267,13 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
   p.lse = d.LSE;
   p.o = d.O;
   p.trace = trace;
-  int max_stages = (SMEM_LIMIT - (int)a128_smem_bytes(DH, 0)) / (int)a128_kv_bytes(DH);
+  auto smem_bytes = [](int stages) { return PSMEM ? aps_smem_bytes(DH, stages) : a128_smem_bytes(DH, stages); };
+  int max_stages = (SMEM_LIMIT - (int)smem_bytes(0)) / (int)a128_kv_bytes(DH);
   if (max_stages > A128_MAX_STAGES) max_stages = A128_MAX_STAGES;
   p.kv_stages = d.D > 0 ? d.D : max_stages;
   if (p.kv_stages < 2)
     return fail(WS_PIPELINE_INFEASIBLE, "the K/V aref needs D >= 2 (ref pipeline.hpp:309-315)");
-  const uint32_t smem = a128_smem_bytes(DH, p.kv_stages);
+  const uint32_t smem = smem_bytes(p.kv_stages);
   if (p.kv_stages > A128_MAX_STAGES || (int)smem > SMEM_LIMIT)
     return fail(WS_SMEM_OVERFLOW, "D=" + std::to_string(p.kv_stages) + " K/V stages need " + std::to_string(smem) +
                                       " B of shared memory; limit " + std::to_string(SMEM_LIMIT));
@@ -279,7 +282,22 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
   if ((s = make_tmap(&tq, d.Q, dt, rows, DH, DH, A128_BM, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
   if ((s = make_tmap(&tk, d.K, dt, rows, DH, DH, A128_BN, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
   if ((s = make_tmap(&tv, d.V, dt, rows, DH, DH, A128_BN, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
-  auto kern = ws_attn128_kernel<DH, BF16>;
+  // WS_ATTN_POLY (developer knob for the exp-mix sweep, bf16 only): column pairs of every 8 whose
+  // exponential runs on the FMA pipe instead of MUFU
+  static const int poly_env = [] {
+    const char* e = getenv("WS_ATTN_POLY");
+    return e ? atoi(e) : -1;
+  }();
+  auto kern = trace ? ws_attn128_kernel<DH, BF16, A128_POLY, true> : ws_attn128_kernel<DH, BF16, A128_POLY>;
+  if (PSMEM) kern = trace ? ws_attn_psmem_kernel<DH, BF16, A128_POLY, true> : ws_attn_psmem_kernel<DH, BF16, A128_POLY>;
+  if (BF16 && !trace) {
+    switch (poly_env) {
+      case 1: kern = PSMEM ? ws_attn_psmem_kernel<DH, BF16, 1> : ws_attn128_kernel<DH, BF16, 1>; break;
+      case 2: kern = PSMEM ? ws_attn_psmem_kernel<DH, BF16, 2> : ws_attn128_kernel<DH, BF16, 2>; break;
+      case 3: kern = PSMEM ? ws_attn_psmem_kernel<DH, BF16, 3> : ws_attn128_kernel<DH, BF16, 3>; break;
+      default: break;
+    }
+  }
   WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = p.bh_fast ? dim3(bh1 - bh0, p.num_pairs) : dim3(p.num_pairs, bh1 - bh0);
@@ -306,11 +324,26 @@ ws_status attn_entry(const ws_attn_desc& d, cudaStream_t st, unsigned long long*
   if (d.kv_block != 0 && d.kv_block != 64 && d.kv_block != 128)
     return fail(WS_TYPE, "kv_block must be 0 (auto), 64 or 128");
   if (d.kv_block != 64) {
+    // P staging: hdim 128 stages P in shared memory (S released early, QK_{j+1} overlaps the
+    // softmax); hdim 64 keeps P in TMEM (its shared-memory P tiles would leave less room for the
+    // K/V ring and its PV is operand-bound in SS form). WS_ATTN_PTMEM=0/1 overrides (developer knob).
+    static const int ptmem_env = [] {
+      const char* e = getenv("WS_ATTN_PTMEM");
+      return e ? atoi(e) : -1;
+    }();
+    const bool ptmem = ptmem_env >= 0 ? ptmem_env == 1 : d.Dh == 64;
+    if (ptmem) {
+      if (d.Dh == 128)
+        return d.dtype == WS_BF16 ? launch_attn128<128, true, false>(d, bh0, bh1, st, trace)
+                                  : launch_attn128<128, false, false>(d, bh0, bh1, st, trace);
+      return d.dtype == WS_BF16 ? launch_attn128<64, true, false>(d, bh0, bh1, st, trace)
+                                : launch_attn128<64, false, false>(d, bh0, bh1, st, trace);
+    }
     if (d.Dh == 128)
-      return d.dtype == WS_BF16 ? launch_attn128<128, true>(d, bh0, bh1, st, trace)
-                                : launch_attn128<128, false>(d, bh0, bh1, st, trace);
-    return d.dtype == WS_BF16 ? launch_attn128<64, true>(d, bh0, bh1, st, trace)
-                              : launch_attn128<64, false>(d, bh0, bh1, st, trace);
+      return d.dtype == WS_BF16 ? launch_attn128<128, true, true>(d, bh0, bh1, st, trace)
+                                : launch_attn128<128, false, true>(d, bh0, bh1, st, trace);
+    return d.dtype == WS_BF16 ? launch_attn128<64, true, true>(d, bh0, bh1, st, trace)
+                              : launch_attn128<64, false, true>(d, bh0, bh1, st, trace);
   }
   if (d.Dh == 128)
     return d.dtype == WS_BF16 ? launch_attn<128, true>(d, bh0, bh1, st, trace)

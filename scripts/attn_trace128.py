@@ -1,0 +1,40 @@
+"""Device timeline of one CTA of the 128-key FA kernel (ws_attn_fwd_traced, kv_block=128).
+
+MMA events per step j: 0 start, 1 K_{j+1}/V_j acquired, 2 p_full[0] passed, 3 PV_0+QK_0 issued,
+4 p_full[1] passed, 5 PV_1+QK_1 issued. Softmax (tile t, warp 4t lane 0): 0 wait start, 1 S_t
+full, 2 S loaded, 3 max (+ correction) done, 4 P stored, 5 p_full arrived."""
+import os, statistics, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2510_14719_b200 as ws
+
+
+def run(S=16384, Dh=128, causal=False, B=1, H=16):
+    q = torch.randn(B, H, S, Dh, device="cuda", dtype=torch.bfloat16); k = torch.randn_like(q); v = torch.randn_like(q)
+    tr = torch.zeros(3 * 256 * 8, dtype=torch.int64, device="cuda")
+    for _ in range(3):
+        ws.attn_fwd(q, k, v, causal=causal, trace=tr, kv_block=128)
+    torch.cuda.synchronize()
+    t = tr.view(3, 256, 8).cpu()
+    n = min(S // 128, 256)
+    if causal:
+        n = min(n, 4)  # CTA (0,0) of the causal grid is the heaviest pair of head 0
+    per = []
+    for j in range(2, n - 1):
+        m, s0, s1 = t[0, j], t[1, j], t[2, j]
+        per.append(dict(
+            step=int(t[0, j + 1, 0] - m[0]), mma_kv=int(m[1] - m[0]), mma_wait_p0=int(m[2] - m[1]),
+            mma_iss0=int(m[3] - m[2]), mma_wait_p1=int(m[4] - m[3]), mma_iss1=int(m[5] - m[4]),
+            sm0_wait=int(s0[1] - s0[0]), sm0_ld=int(s0[2] - s0[1]), sm0_max=int(s0[3] - s0[2]),
+            sm0_exp=int(s0[4] - s0[3]), sm0_arr=int(s0[5] - s0[4]),
+            sm1_wait=int(s1[1] - s1[0]), sm1_ld=int(s1[2] - s1[1]), sm1_max=int(s1[3] - s1[2]),
+            sm1_exp=int(s1[4] - s1[3]), s1_minus_s0=int(s1[1] - s0[1])))
+    if not per:
+        print("too few steps"); return
+    print(f"S={S} Dh={Dh} causal={causal} POLY={os.environ.get('WS_ATTN_POLY', 'default')} steps={len(per)}")
+    print("  median:", {k: statistics.median(r[k] for r in per) for k in per[0]})
+
+
+if __name__ == "__main__":
+    run()
+    run(Dh=64)

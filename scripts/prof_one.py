@@ -12,6 +12,7 @@ ap.add_argument("--bn", type=int, default=0)
 ap.add_argument("--D", type=int, default=0)
 ap.add_argument("--P", type=int, default=0)
 ap.add_argument("--cta_pair", action="store_true")
+ap.add_argument("--kvb", type=int, default=0)
 a = ap.parse_args()
 dev = torch.device("cuda")
 if a.what.startswith("gemm"):
@@ -24,6 +25,6 @@ else:
     Dh = 64 if a.what == "attn_causal64" else 128
     q = torch.randn(1, 16, 16384, Dh, device=dev, dtype=torch.bfloat16); k = torch.randn_like(q); v = torch.randn_like(q)
     for _ in range(a.n):
-        ws.attn_fwd(q, k, v, causal=a.what != "attn", D=a.D)
+        ws.attn_fwd(q, k, v, causal=a.what != "attn", D=a.D, kv_block=a.kvb)
 torch.cuda.synchronize()
 print("done", a)

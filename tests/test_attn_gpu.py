@@ -38,41 +38,58 @@ def _check(q, k, v, o, lse, causal, pid_range=None, block=128):
     return err_o, err_l
 
 
+KV_BLOCKS = [128, 64]  # 128: attn_psmem (hdim 128) / attn128 (hdim 64) kernels; 64: attn_sm100.cuh
+
+
+@pytest.mark.parametrize("kv_block", KV_BLOCKS)
 @pytest.mark.parametrize("Dh", [64, 128])
 @pytest.mark.parametrize("causal", [False, True])
 @pytest.mark.parametrize("dt", [BF16, F16])
-def test_small_parity(ws, dev, Dh, causal, dt):
+def test_small_parity(ws, dev, Dh, causal, dt, kv_block):
     q, k, v = _inputs(1, 2, 512, Dh, dt, dev)
-    o, lse = ws.attn_fwd(q, k, v, causal=causal)
+    o, lse = ws.attn_fwd(q, k, v, causal=causal, kv_block=kv_block)
     torch.cuda.synchronize()
     _check(q, k, v, o, lse, causal)
 
 
+@pytest.mark.parametrize("kv_block", KV_BLOCKS)
+@pytest.mark.parametrize("Dh", [64, 128])
 @pytest.mark.parametrize("causal", [False, True])
-def test_full_range_scores(ws, dev, causal):
+def test_full_range_scores(ws, dev, causal, Dh, kv_block):
     """Unscaled reference inputs: score std ~5.7 after 1/sqrt(Dh), so the running max
     moves by far more than the lazy-rescale threshold and the correction path runs."""
-    q, k, v = _inputs(2, 2, 1024, 128, BF16, dev, qk_div=1.0)
-    o, lse = ws.attn_fwd(q, k, v, causal=causal)
+    q, k, v = _inputs(2, 2, 1024, Dh, BF16, dev, qk_div=1.0)
+    o, lse = ws.attn_fwd(q, k, v, causal=causal, kv_block=kv_block)
     torch.cuda.synchronize()
     _check(q, k, v, o, lse, causal)
 
 
-@pytest.mark.parametrize("D", [2, 3, 4])
-def test_kv_aref_depths(ws, dev, D):
-    q, k, v = _inputs(1, 2, 768, 128, BF16, dev)
-    o, lse = ws.attn_fwd(q, k, v, causal=True, D=D)
+@pytest.mark.parametrize("kv_block,D", [(64, 2), (64, 3), (64, 4), (128, 2), (128, 3)])
+@pytest.mark.parametrize("Dh", [64, 128])
+def test_kv_aref_depths(ws, dev, D, kv_block, Dh):
+    q, k, v = _inputs(1, 2, 768, Dh, BF16, dev)
+    o, lse = ws.attn_fwd(q, k, v, causal=True, D=D, kv_block=kv_block)
     torch.cuda.synchronize()
     _check(q, k, v, o, lse, True)
 
 
-def test_softmax_rows_sum_to_one(ws, dev):
+def test_kv_aref_depth_over_smem_is_rejected(ws, dev):
+    """hdim 128 with P staged in shared memory leaves room for 3 K/V slots: D=4 is SMEM_OVERFLOW
+    (the reference's smem gate, ref proj/include/warpspec/sim.hpp:81-84, against the real limit)."""
+    q, k, v = _inputs(1, 2, 768, 128, BF16, dev)
+    with pytest.raises(ws.WsError) as e:
+        ws.attn_fwd(q, k, v, causal=True, D=4)
+    assert e.value.code == "smem-overflow"
+
+
+@pytest.mark.parametrize("kv_block", KV_BLOCKS)
+def test_softmax_rows_sum_to_one(ws, dev, kv_block):
     """Size-independent property: with V = 1 every output row is sum(p)/l = 1."""
     B, H, S, Dh = 1, 4, 2048, 128
     q, k, _ = _inputs(B, H, S, Dh, BF16, dev, qk_div=1.0)
     v = torch.ones_like(q)
     for causal in (False, True):
-        o, _ = ws.attn_fwd(q, k, v, causal=causal)
+        o, _ = ws.attn_fwd(q, k, v, causal=causal, kv_block=kv_block)
         torch.cuda.synchronize()
         assert (o.float() - 1).abs().max().item() <= 1e-2
 

@@ -85,6 +85,9 @@ def _attn_desc(ws, **kw):
     (dict(Dh=96), "unsupported-kernel"),
     (dict(D=1), "pipeline-infeasible"),             # coarse schedule needs D >= 2 (ref pipeline.hpp:309-315)
     (dict(D=9), "smem-overflow"),
+    (dict(D=4), "smem-overflow"),                   # hdim 128, P in shared memory: room for 3 K/V slots
+    (dict(D=9, kv_block=64), "smem-overflow"),
+    (dict(kv_block=96), "type"),
     (dict(dtype=3), "type"),
     (dict(bh_begin=1, bh_end=1), "type"),
 ])
