@@ -78,7 +78,8 @@ typedef struct ws_gemm_desc {
   int32_t P;                   /* MMA k-blocks in flight; 0 = D (commit straight to empty) */
   int32_t persistent;          /* 1 = one CTA per SM looping over tiles; 0 = one CTA per tile */
   int32_t cta_pair;            /* 1 = cta_group::2 256-row tiles (cooperative WGs analogue) */
-  int32_t bn;                  /* N tile: 0 = auto, else 128 or 256 */
+  int32_t bn;                  /* N tile: 0 = auto, else 128, 256 or 512 (512: cta_pair only, a
+                                  256 x 512 pair tile with one TMEM accumulator) */
   int32_t group_m;             /* raster: tiles grouped by this many M-blocks; 0 = auto */
   int32_t act;                 /* epilogue activation: 0 none, 1 relu (gemm_act.k, ref
                                   proj/kernels/gemm_act.k:10-16) */

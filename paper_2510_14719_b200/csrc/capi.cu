@@ -139,7 +139,9 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
     return fail(WS_SMEM_OVERFLOW, "D=" + std::to_string(p.stages) + " stages need " + std::to_string(L.total) +
                                       " B of shared memory; limit " + std::to_string(SMEM_LIMIT));
   // raster groups are counted in scheduling M-blocks (256 rows for a CTA pair)
-  p.group_m = d.group_m > 0 ? d.group_m : 16 / CG;
+  // auto raster (measured on B200, scripts/gemm_ab.py): 256 x 512 pair tiles in groups of 16
+  // M-blocks, 256 x 256 pair tiles in groups of 2, single-CTA tiles in groups of 4
+  p.group_m = d.group_m > 0 ? d.group_m : (BN == 512 ? 16 : CG == 2 ? 2 : 4);
   if (p.group_m > p.num_m_blocks / CG) p.group_m = p.num_m_blocks / CG;
   p.scale = d.scale_a * d.scale_b;
   p.act = d.act;
@@ -148,7 +150,8 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   ws_status s;
   if ((s = make_tmap(&ta, d.A, in_dt, d.M, d.K, d.lda, GEMM_BM, kbox, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
     return s;
-  if ((s = make_tmap(&tb, d.B, in_dt, d.N, d.K, d.ldb, BN / CG, kbox, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
+  if ((s = make_tmap(&tb, d.B, in_dt, d.N, d.K, d.ldb, (BN > 256 ? 256 : BN) / CG, kbox,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
     return s;
   const int cw = 128 / elem_bytes(out_dt);
   if ((s = make_tmap(&tc, d.C, out_dt, d.M, d.N, d.ldc, 32, cw, CU_TENSOR_MAP_L2_PROMOTION_NONE)) != WS_OK) return s;
@@ -179,6 +182,15 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
 
 template <int IN, int BN>
 ws_status dispatch_out(const ws_gemm_desc& d, cudaStream_t st) {
+  if constexpr (BN == 512) {
+    // 256 x 512 pair tiles exist only as cta_group::2 (checked by the caller)
+    switch (d.out_dtype) {
+      case WS_F32: return launch_gemm<IN, ws::OUT_F32, BN, 2>(d, st);
+      case WS_BF16: return launch_gemm<IN, ws::OUT_BF16, BN, 2>(d, st);
+      case WS_F16: return launch_gemm<IN, ws::OUT_F16, BN, 2>(d, st);
+    }
+    return fail(WS_TYPE, "out_dtype must be F32, BF16 or F16");
+  }
   if (d.cta_pair) {
     switch (d.out_dtype) {
       case WS_F32: return launch_gemm<IN, ws::OUT_F32, BN, 2>(d, st);
@@ -373,8 +385,13 @@ ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
                 "MMA pipelining depth P=" + std::to_string(d.P) + " exceeds aref depth D=" + std::to_string(d.D));
   const int eb = elem_bytes(d.in_dtype);
   if (eb == 0 || d.in_dtype == WS_F32) return fail(WS_TYPE, "in_dtype must be F16, BF16 or E4M3");
-  int bn = d.bn > 0 ? d.bn : 256;
-  if (bn != 128 && bn != 256) return fail(WS_TYPE, "bn must be 128 or 256");
+  // auto N tile: a 256 x 512 pair tile moves 25% fewer operand bytes per output than 256 x 256
+  // (what keeps the power-capped clock up on long K), but its single TMEM accumulator leaves the
+  // epilogue unoverlapped — worth it once the mainloop is >= 64 K-blocks
+  const int64_t kblocks = d.K / (128 / (eb > 0 ? eb : 1));
+  int bn = d.bn > 0 ? d.bn : (d.cta_pair && kblocks >= 64 && d.N % 512 == 0) ? 512 : 256;
+  if (bn != 128 && bn != 256 && bn != 512) return fail(WS_TYPE, "bn must be 128, 256 or 512");
+  if (bn == 512 && !d.cta_pair) return fail(WS_TYPE, "bn=512 (256 x 512 tiles) needs cta_pair=1");
   const int bm = d.cta_pair ? 2 * ws::GEMM_BM : ws::GEMM_BM;
   if (d.M % bm) return fail(WS_INDIVISIBLE_TILE, "M=" + std::to_string(d.M) + " is not a multiple of " + std::to_string(bm));
   if (d.N % bn) return fail(WS_INDIVISIBLE_TILE, "N=" + std::to_string(d.N) + " is not a multiple of bn=" + std::to_string(bn));
@@ -382,7 +399,7 @@ ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
     return fail(WS_INDIVISIBLE_TILE, "K=" + std::to_string(d.K) + " is not a multiple of " + std::to_string(128 / eb));
   if (d.lda < d.K || d.ldb < d.K || d.ldc < d.N) return fail(WS_TYPE, "leading dimension smaller than the row");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
-  return bn == 256 ? dispatch_in<256>(d, st) : dispatch_in<128>(d, st);
+  return bn == 512 ? dispatch_in<512>(d, st) : bn == 256 ? dispatch_in<256>(d, st) : dispatch_in<128>(d, st);
 }
 
 ws_status ws_attn_fwd(const ws_attn_desc* desc, void* cuda_stream) {

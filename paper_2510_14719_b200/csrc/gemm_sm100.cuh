@@ -80,12 +80,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     ws_gemm_tn_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_constant__ CUtensorMap tm_b,
                       const __grid_constant__ CUtensorMap tm_c, const GemmParams p) {
   constexpr int BN_LOCAL = BN / CG;
-  constexpr uint32_t TMEM_COLS = 2 * BN <= 256 ? 256 : 512;  // two accumulator buffers
+  // BN = 512 (a 256 x 512 pair tile, 25% fewer operand bytes per output than 256 x 256): two
+  // N = 256 MMAs per K step and a single TMEM accumulator; otherwise two accumulator buffers.
+  constexpr int MMA_N = BN > 256 ? 256 : BN;
+  constexpr int NH = BN / MMA_N;                        // N halves per K step
+  constexpr int B_BOX = MMA_N / CG;                     // B rows per CTA per half
+  constexpr int ACC = 2 * BN <= 512 ? 2 : 1;            // accumulator buffers in TMEM
+  constexpr uint32_t TMEM_COLS = ACC * BN <= 256 ? 256 : 512;
   constexpr int OUT_BYTES = OUT == OUT_F32 ? 4 : 2;
   constexpr int CW = 128 / OUT_BYTES;  // epilogue chunk: output columns per 128-byte row
   constexpr int UMMA_K_BYTES = 32;     // 16 x 16-bit or 32 x 8-bit per tcgen05.mma
   constexpr int KSTEPS = GEMM_ROW_BYTES / UMMA_K_BYTES;
-  constexpr uint32_t IDESC = make_idesc(IN == IN_BF16 ? 1u : 0u, GEMM_BM * CG, BN, 0, 0);
+  constexpr uint32_t IDESC = make_idesc(IN == IN_BF16 ? 1u : 0u, GEMM_BM * CG, MMA_N, 0, 0);
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -108,7 +114,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch_desc(&tm_b);
     tma_prefetch_desc(&tm_c);
     ring->init(D, 1, 1);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < ACC; ++i) {
       mbar_init(&tmem_full[i], 1);
       mbar_init(&tmem_empty[i], 4 * CG);  // one arrival per epilogue warp of every CTA in the pair
     }
@@ -133,7 +139,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         int mb, nb;
         gemm_tile_coords(t, p, p.num_m_blocks / CG, mb, nb);
         const int arow = mb * GEMM_BM * CG + static_cast<int>(rank) * GEMM_BM;
-        const int brow = nb * BN + static_cast<int>(rank) * BN_LOCAL;
+        const int brow = nb * BN + static_cast<int>(rank) * B_BOX;  // + h * MMA_N for half h
         for (int kb = 0; kb < p.num_k_blocks; ++kb) {
           ring->put_acquire(c, 1);
           uint8_t* sa = smem + c.slot * L.stage_bytes;
@@ -143,12 +149,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           if constexpr (CG == 1) {
             ring->put_expect(c, L.stage_bytes);
             tma_load_2d(sa, &tm_a, &ring->full[c.slot], kcoord, arow);
-            tma_load_2d(sb, &tm_b, &ring->full[c.slot], kcoord, brow);
+#pragma unroll
+            for (int h = 0; h < NH; ++h)
+              tma_load_2d(sb + h * B_BOX * GEMM_ROW_BYTES, &tm_b, &ring->full[c.slot], kcoord, brow + h * MMA_N);
           } else {
             // the leader's full barrier collects both CTAs' bytes (one expect_tx for the pair)
             if (leader) ring->put_expect(c, 2 * L.stage_bytes);
             tma_load_2d_cg2(sa, &tm_a, &ring->full[c.slot], kcoord, arow);
-            tma_load_2d_cg2(sb, &tm_b, &ring->full[c.slot], kcoord, brow);
+#pragma unroll
+            for (int h = 0; h < NH; ++h)
+              tma_load_2d_cg2(sb + h * B_BOX * GEMM_ROW_BYTES, &tm_b, &ring->full[c.slot], kcoord, brow + h * MMA_N);
           }
           c.advance(D);
         }
@@ -178,11 +188,14 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 #pragma unroll
           for (int k = 0; k < KSTEPS; ++k) {
             const uint64_t ad = make_sw128_desc(sa + k * UMMA_K_BYTES, 16, 1024);
-            const uint64_t bd = make_sw128_desc(sb + k * UMMA_K_BYTES, 16, 1024);
-            if constexpr (IN == IN_E4M3)
-              mma_f8_ss<CG>(d_tmem, ad, bd, IDESC, (kb | k) != 0);
-            else
-              mma_f16_ss<CG>(d_tmem, ad, bd, IDESC, (kb | k) != 0);
+#pragma unroll
+            for (int h = 0; h < NH; ++h) {
+              const uint64_t bd = make_sw128_desc(sb + h * B_BOX * GEMM_ROW_BYTES + k * UMMA_K_BYTES, 16, 1024);
+              if constexpr (IN == IN_E4M3)
+                mma_f8_ss<CG>(d_tmem + h * MMA_N, ad, bd, IDESC, (kb | k) != 0);
+              else
+                mma_f16_ss<CG>(d_tmem + h * MMA_N, ad, bd, IDESC, (kb | k) != 0);
+            }
           }
           if constexpr (CG == 1)
             ring->consumed_by_mma(c);
@@ -195,7 +208,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mma_commit(&tmem_full[acc_stage]);
         else
           mma_commit_mc2(&tmem_full[acc_stage], 0x3);
-        if (++acc_stage == 2) {
+        if (++acc_stage == ACC) {
           acc_stage = 0;
           acc_phase ^= 1u;
         }
@@ -276,7 +289,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tma_store_commit();
         }
       }
-      if (++acc_stage == 2) {
+      if (++acc_stage == ACC) {
         acc_stage = 0;
         acc_phase ^= 1u;
       }
