@@ -270,6 +270,7 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
   p.S = d.S;
   p.BH_begin = bh0;
   p.num_pairs = d.S / (2 * A128_BM);
+  p.num_bh = bh1 - bh0;
   p.causal = d.causal;
   // causal: (b,h) fastest so every head's heaviest query pairs run first (longest-first);
   // non-causal: the query pairs of one (b,h) run together and share its K/V in L2
@@ -312,7 +313,18 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
   }
   WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = p.bh_fast ? dim3(bh1 - bh0, p.num_pairs) : dim3(p.num_pairs, bh1 - bh0);
+  if (PSMEM) {
+    // persistent: one CTA per SM over the (pair, (b,h)) items (attn_psmem_sm100.cuh);
+    // WS_ATTN_PERSIST=0 (developer knob) launches one CTA per item instead
+    static const int persist_env = [] {
+      const char* e = getenv("WS_ATTN_PERSIST");
+      return e ? atoi(e) : 1;
+    }();
+    const int items = p.num_pairs * p.num_bh;
+    cfg.gridDim = dim3(persist_env == 0 || items < num_sms() ? items : num_sms());
+  } else {
+    cfg.gridDim = p.bh_fast ? dim3(bh1 - bh0, p.num_pairs) : dim3(p.num_pairs, bh1 - bh0);
+  }
   cfg.blockDim = dim3(A128_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;

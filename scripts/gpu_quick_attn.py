@@ -55,6 +55,10 @@ if __name__ == "__main__":
         check(1, 2, 512, 64, True, kv_block=kb)
         check(2, 3, 1024, 128, False, dt=torch.float16, kv_block=kb)
         check(1, 2, 1024, 128, True, scale_in=0.25, kv_block=kb)
+        # several work items per CTA (the persistent kernels loop over items)
+        check(4, 16, 2048, 128, False, kv_block=kb)
+        check(4, 16, 2048, 128, True, kv_block=kb)
+        check(2, 16, 2048, 64, True, kv_block=kb)
         for D in (2, 3, 4, 5):
             check(1, 2, 1024, 128, True, D=D, kv_block=kb)
             check(1, 2, 1024, 64, False, D=D, kv_block=kb)
