@@ -10,7 +10,9 @@
 //   warp 1      MMA issuer: get -> BK/UMMA_K tcgen05.mma into a TMEM accumulator -> consumed
 //               by tcgen05.commit; the accumulator is itself a depth-2 aref (TMEM full/empty)
 //   warp 2      TMEM allocator
-//   warps 4..7  epilogue: tcgen05.ld -> scale/convert -> swizzled smem -> TMA store
+//   warps 4..11 epilogue: tcgen05.ld -> scale/convert -> swizzled smem -> TMA store; two warps per
+//               TMEM lane quarter (warp w reads lanes 32*(w%4)..), each draining half the columns,
+//               with the next chunk's TMEM load in flight while the current one is converted
 // Persistent scheduling (ref proj/include/warpspec/grid.hpp:93-123, run_grid :140-210): tile t
 // runs on CTA t mod gridDim.x; no per-tile barrier reset or quiesce — the aref phases carry over.
 #pragma once
@@ -22,9 +24,10 @@ namespace ws {
 constexpr int GEMM_BM = 128;           // rows per CTA tile (one TMEM lane per row)
 constexpr int GEMM_ROW_BYTES = 128;    // one 128-byte swizzle row of K per stage
 constexpr int GEMM_MAX_STAGES = 8;
-constexpr int GEMM_THREADS = 256;      // 8 warps
+constexpr int GEMM_THREADS = 384;      // 12 warps
 constexpr int GEMM_EPI_WARP0 = 4;
-constexpr int GEMM_EPI_BUF_BYTES = 32 * 128;  // per epilogue warp per buffer: 32 rows x 128 B
+constexpr int GEMM_EPI_WARPS = 8;      // two per TMEM lane quarter, each draining half the columns
+constexpr int GEMM_EPI_BUF_BYTES = 32 * 128;  // per epilogue warp: 32 rows x 128 B staging buffer
 
 enum InFmt : int { IN_F16 = 0, IN_BF16 = 1, IN_E4M3 = 2 };
 enum OutFmt : int { OUT_F32 = 0, OUT_BF16 = 1, OUT_F16 = 2 };
@@ -50,7 +53,7 @@ __host__ __device__ inline GemmSmemLayout gemm_smem_layout(int bn_local, int sta
   L.b_bytes = bn_local * GEMM_ROW_BYTES;
   L.stage_bytes = L.a_bytes + L.b_bytes;
   L.epi_offset = stages * L.stage_bytes;
-  L.bar_offset = L.epi_offset + 4 * 2 * GEMM_EPI_BUF_BYTES;
+  L.bar_offset = L.epi_offset + GEMM_EPI_WARPS * GEMM_EPI_BUF_BYTES;
   // full[MAX], empty[MAX], tmem_full[2], tmem_empty[2], tmem base word
   L.total = L.bar_offset + (2 * GEMM_MAX_STAGES + 4) * 8 + 16 + 1024 /* alignment slack */;
   return L;
@@ -116,7 +119,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     ring->init(D, 1, 1);
     for (int i = 0; i < ACC; ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], 4 * CG);  // one arrival per epilogue warp of every CTA in the pair
+      mbar_init(&tmem_empty[i], GEMM_EPI_WARPS * CG);  // one arrival per epilogue warp of every CTA in the pair
     }
     fence_barrier_init();
   } else if (warp == 2) {
@@ -216,29 +219,32 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     }
   } else if (warp >= GEMM_EPI_WARP0) {
     // ===================== epilogue: TMEM -> regs -> smem -> TMA store =====================
-    const uint32_t q = warp & 3u;  // TMEM lane quarter this warp may access
-    uint8_t* stage_base = smem + L.epi_offset + q * 2 * GEMM_EPI_BUF_BYTES;
-    uint32_t acc_stage = 0, acc_phase = 0, chunk_ctr = 0;
+    const uint32_t q = warp & 3u;                          // TMEM lane quarter this warp may access
+    const int hc = static_cast<int>(warp - GEMM_EPI_WARP0) >> 2;  // column half
+    constexpr int NCHW = BN / 2 / CW;                      // chunks per warp per tile
+    uint8_t* buf = smem + L.epi_offset + (warp - GEMM_EPI_WARP0) * GEMM_EPI_BUF_BYTES;
+    const uint32_t row_addr = smem_u32(buf) + lane * 128u;  // row `lane` of this warp's 32-row slab
+    uint32_t acc_stage = 0, acc_phase = 0, stores = 0;
     const float scale = p.scale;
-    const float lo_clamp = p.act == 1 ? 0.f : -INFINITY;  // relu epilogue (gemm_act.k)
+    const bool plain = p.scale == 1.f && p.act == 0;        // no scale / activation: convert only
+    const float lo_clamp = p.act == 1 ? 0.f : -INFINITY;   // relu epilogue (gemm_act.k)
+    auto tmem_load = [&](uint32_t taddr, uint32_t(&v)[CW]) {
+      tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
+      if constexpr (CW == 64) tmem_ld32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+    };
     for (int t = tile0; t < num_tiles; t += tile_stride) {
       int mb, nb;
       gemm_tile_coords(t, p, p.num_m_blocks / CG, mb, nb);
       const int crow = mb * GEMM_BM * CG + static_cast<int>(rank) * GEMM_BM;
       mbar_wait(&tmem_full[acc_stage], acc_phase, 5);
       tc_fence_after();
-      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc_stage * BN;
-#pragma unroll 1
-      for (int ch = 0; ch < BN / CW; ++ch, ++chunk_ctr) {
-        uint32_t v[CW];
-        if constexpr (CW == 64) {
-          tmem_ld32(t_row + ch * CW, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-          tmem_ld32(t_row + ch * CW + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
+      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc_stage * BN + hc * (BN / 2);
+      // one chunk: CW columns = 128 bytes of output per row
+      auto chunk = [&](uint32_t(&cur)[CW], uint32_t(&nxt)[CW], int ch) {
+        tmem_wait_ld();  // cur landed
+        if (ch + 1 < NCHW) {
+          tmem_load(t_row + (ch + 1) * CW, nxt);  // in flight while cur is converted and stored
         } else {
-          tmem_ld32(t_row + ch * CW, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
-        }
-        tmem_wait_ld();
-        if (ch == BN / CW - 1) {
           // accumulator fully read: release it to the MMA warp (accumulator aref consumed)
           tc_fence_before();
           __syncwarp();
@@ -249,45 +255,43 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
               mbar_arrive_cluster(&tmem_empty[acc_stage], 0);  // the leader's MMA warp owns the release
           }
         }
-        uint8_t* buf = stage_base + (chunk_ctr & 1u) * GEMM_EPI_BUF_BYTES;
-        if (chunk_ctr >= 2) {
-          if (lane == 0) tma_store_wait_read<1>();  // the store that last used this buffer has read it
+        uint32_t w[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if constexpr (OUT == OUT_F32) {
+            const float f = __uint_as_float(cur[j]);
+            w[j] = plain ? cur[j] : __float_as_uint(fmaxf(f * scale, lo_clamp));
+          } else {
+            float f0 = __uint_as_float(cur[2 * j]), f1 = __uint_as_float(cur[2 * j + 1]);
+            if (!plain) {
+              f0 = fmaxf(f0 * scale, lo_clamp);
+              f1 = fmaxf(f1 * scale, lo_clamp);
+            }
+            w[j] = OUT == OUT_BF16 ? pack_bf16(f0, f1) : pack_f16(f0, f1);
+          }
+        }
+        if (stores > 0) {
+          if (lane == 0) tma_store_wait_read<0>();  // the previous store has read the staging buffer
           __syncwarp();
         }
-        // row `lane` of this warp's 32-row slab: 8 x 16-byte chunks, 128B-swizzled
-        const uint32_t row_addr = smem_u32(buf) + lane * 128u;
+        // 8 x 16-byte chunks per row, 128B-swizzled
 #pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          uint32_t w0, w1, w2, w3;
-          if constexpr (OUT == OUT_F32) {
-            w0 = __float_as_uint(fmaxf(__uint_as_float(v[4 * j + 0]) * scale, lo_clamp));
-            w1 = __float_as_uint(fmaxf(__uint_as_float(v[4 * j + 1]) * scale, lo_clamp));
-            w2 = __float_as_uint(fmaxf(__uint_as_float(v[4 * j + 2]) * scale, lo_clamp));
-            w3 = __float_as_uint(fmaxf(__uint_as_float(v[4 * j + 3]) * scale, lo_clamp));
-          } else {
-            float f[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) f[e] = fmaxf(__uint_as_float(v[8 * j + e]) * scale, lo_clamp);
-            if constexpr (OUT == OUT_BF16) {
-              w0 = pack_bf16(f[0], f[1]);
-              w1 = pack_bf16(f[2], f[3]);
-              w2 = pack_bf16(f[4], f[5]);
-              w3 = pack_bf16(f[6], f[7]);
-            } else {
-              w0 = pack_f16(f[0], f[1]);
-              w1 = pack_f16(f[2], f[3]);
-              w2 = pack_f16(f[4], f[5]);
-              w3 = pack_f16(f[6], f[7]);
-            }
-          }
-          st_shared_v4(row_addr + ((j ^ (lane & 7u)) << 4), w0, w1, w2, w3);
-        }
+        for (int j = 0; j < 8; ++j)
+          st_shared_v4(row_addr + ((j ^ (lane & 7u)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&tm_c, buf, nb * BN + ch * CW, crow + q * 32);
+          tma_store_2d(&tm_c, buf, nb * BN + hc * (BN / 2) + ch * CW, crow + q * 32);
           tma_store_commit();
         }
+        ++stores;
+      };
+      uint32_t va[CW], vb[CW];
+      tmem_load(t_row, va);
+#pragma unroll 1
+      for (int ch = 0; ch < NCHW; ch += 2) {
+        chunk(va, vb, ch);
+        if (ch + 1 < NCHW) chunk(vb, va, ch + 1);
       }
       if (++acc_stage == ACC) {
         acc_stage = 0;
