@@ -151,3 +151,24 @@ def test_launches_are_counted(ws, dev):
     n0 = ws.launch_count()
     _run(ws, dev, 128, 256, 64, BF16, F32)
     assert ws.launch_count() == n0 + 1
+
+
+def test_host_pipeline_matches_device_path_bit_exact(ws, dev):
+    """gemm_tn_host (host buffers, H2D / GEMM / D2H overlapped on three streams, slots reused every
+    other job) gives the oracle's exact fp32 results for every job, across two calls."""
+    shapes = [(256, 512, 128), (512, 256, 1024), (256, 256, 64), (512, 512, 256), (256, 768, 512)]
+    jobs, want = [], []
+    for i, (M, N, K) in enumerate(shapes):
+        a = oracle.generate_real(f"a{i}", (M, K))
+        b = oracle.generate_real(f"b{i}", (N, K))
+        jobs.append((torch.from_numpy(a).to(torch.bfloat16).pin_memory(),
+                     torch.from_numpy(b).to(torch.bfloat16).pin_memory(),
+                     torch.full((M, N), float("nan"), dtype=torch.float32).pin_memory()))
+        want.append(oracle.gemm(a, b))
+    for _ in range(2):
+        for _, _, c in jobs:
+            c.fill_(float("nan"))
+        ev = ws.gemm_tn_host(jobs, device=dev)
+        ev.synchronize()
+        for (_, _, c), w in zip(jobs, want):
+            assert np.array_equal(c.numpy().astype(np.float64), w)
