@@ -37,6 +37,7 @@ constexpr int A128_POLY = 2;          // default exp mix: 2 of every 8 column pa
 struct Attn128Params {
   int S, BH_begin, num_pairs;  // num_pairs = S / 256 work items per (b,h)
   int num_bh;                  // (b,h) slices in this launch (the persistent kernel's item space)
+  int stagger;                 // attn_psmem: issue QK_1(j+1) after PV_0(j) (offsets the two tiles)
   int kv_stages;
   int causal;
   int bh_fast;        // grid order: 1 = blockIdx.x walks (b,h) (causal, heaviest pairs first);

@@ -37,6 +37,11 @@
 
 namespace ws {
 
+// default exp mix of this kernel: 1 of every 8 column pairs on the FMA pipe. With the staggered
+// issue order (p.stagger) the two softmax warpgroups overlap, so the FMA pipe is the scarcer one
+// (measured, scripts/attn_ab.py: stagger + 1/8 beats 2/8 by 3-4% at hdim 128).
+constexpr int APS_POLY = 1;
+
 __host__ __device__ inline uint32_t aps_smem_bytes(int Dh, int kv_stages) {
   // Q0 | Q1 | P0 | P1 | kv slots | barriers (+1 KB alignment slack)
   return 2 * a128_q_bytes(Dh) + 2 * A128_BM * A128_BN * 2 + kv_stages * a128_kv_bytes(Dh) +
@@ -217,9 +222,19 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       c.advance(D);
       for (int j = 0; j < n1; ++j) {
         if (lane == 0) WS_TRACE(0, j, 0);
-        if (j + 1 < n1) {
+        const bool more = j + 1 < n1;
+        uint32_t kslot = 0;
+        auto qk1 = [&]() {
+          mbar_wait(&s_free[1], (g1 + j) & 1, 18);
+          tc_fence_after();
+          issue_qk(1, kslot);
+          mma_commit_warp(&s_full[1]);
+          mma_commit_warp(&ring->empty[kslot]);
+          if (j + 2 == n1) mma_commit_warp(q_free);  // that was the item's last QK: Q reusable
+        };
+        if (more) {
           ring->get(c, 13);  // K_{j+1}
-          const uint32_t kslot = c.slot;
+          kslot = c.slot;
           c.advance(D);
           if (j + 1 < n0) {
             mbar_wait(&s_free[0], (g0 + j) & 1, 17);  // S_0(j) copied out
@@ -228,12 +243,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
             mma_commit_warp(&s_full[0]);
           }
           if (lane == 0) WS_TRACE(0, j, 1);
-          mbar_wait(&s_free[1], (g1 + j) & 1, 18);
-          tc_fence_after();
-          issue_qk(1, kslot);
-          mma_commit_warp(&s_full[1]);
-          mma_commit_warp(&ring->empty[kslot]);
-          if (j + 2 == n1) mma_commit_warp(q_free);  // that was the item's last QK: Q reusable
+          if (!p.stagger) qk1();
         }
         if (lane == 0) WS_TRACE(0, j, 2);
         ring->get(c, 14);  // V_j
@@ -247,6 +257,10 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
           issue_pv(0, vslot, j > 0);
           mma_commit_warp(&pv_done[0]);
         }
+        // stagger: QK_1(j+1) after PV_0(j), so tile 1's S lands half a step after tile 0's and the
+        // two softmax warpgroups' latency-bound phases (row max) interleave with the other's
+        // exponentials instead of coinciding
+        if (more && p.stagger) qk1();
         mbar_wait(&p_full[1], (g1 + j) & 1, 16);
         if (j == 0 && it > 0) mbar_wait(&o_free[1], (it - 1) & 1, 19);
         tc_fence_after();

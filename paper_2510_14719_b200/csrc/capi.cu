@@ -271,6 +271,11 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
   p.BH_begin = bh0;
   p.num_pairs = d.S / (2 * A128_BM);
   p.num_bh = bh1 - bh0;
+  static const int stagger_env = [] {  // WS_ATTN_STAGGER (developer knob)
+    const char* e = getenv("WS_ATTN_STAGGER");
+    return e ? atoi(e) : 1;
+  }();
+  p.stagger = stagger_env;
   p.causal = d.causal;
   // causal: (b,h) fastest so every head's heaviest query pairs run first (longest-first);
   // non-causal: the query pairs of one (b,h) run together and share its K/V in L2
@@ -302,7 +307,8 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
     return e ? atoi(e) : -1;
   }();
   auto kern = trace ? ws_attn128_kernel<DH, BF16, A128_POLY, true> : ws_attn128_kernel<DH, BF16, A128_POLY>;
-  if (PSMEM) kern = trace ? ws_attn_psmem_kernel<DH, BF16, A128_POLY, true> : ws_attn_psmem_kernel<DH, BF16, A128_POLY>;
+  if (PSMEM)
+    kern = trace ? ws_attn_psmem_kernel<DH, BF16, APS_POLY, true> : ws_attn_psmem_kernel<DH, BF16, APS_POLY>;
   if (BF16 && !trace) {
     switch (poly_env) {
       case 1: kern = PSMEM ? ws_attn_psmem_kernel<DH, BF16, 1> : ws_attn128_kernel<DH, BF16, 1>; break;
