@@ -117,9 +117,11 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tma_prefetch_desc(&tm_b);
     tma_prefetch_desc(&tm_c);
     ring->init(D, 1, 1);
-    for (int i = 0; i < ACC; ++i) {
+    // BN = 512: one barrier pair per N half (the half-by-half hand-over below), each drained by
+    // the four epilogue warps of that column half; otherwise one pair per accumulator buffer
+    for (int i = 0; i < (NH == 2 ? 2 : ACC); ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], GEMM_EPI_WARPS * CG);  // one arrival per epilogue warp of every CTA in the pair
+      mbar_init(&tmem_empty[i], (NH == 2 ? GEMM_EPI_WARPS / 2 : GEMM_EPI_WARPS) * CG);  // per epilogue warp, per CTA
     }
     fence_barrier_init();
   } else if (warp == 2) {
@@ -174,46 +176,111 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t gk = 0;  // global k-block counter (for the literal P window)
       uint32_t acc_stage = 0, acc_phase = 0;
       const uint32_t P = static_cast<uint32_t>(p.mma_depth);
-      for (int t = tile0; t < num_tiles; t += tile_stride) {
-        mbar_wait(&tmem_empty[acc_stage], acc_phase ^ 1u, 3);
-        tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc_stage * BN;
-        for (int kb = 0; kb < p.num_k_blocks; ++kb, ++gk) {
-          if (P < D && gk >= P) {
-            // at most P k-blocks of MMAs in flight (ref pipeline.hpp:98-140, "wait <= P-1")
-            const uint32_t old = gk - P;
-            mbar_wait(&ring->empty[old % D], (old / D) & 1u, 4);
-          }
-          ring->get(c, 2);
-          tc_fence_after();
-          const uint32_t sa = smem_u32(smem + c.slot * L.stage_bytes);
-          const uint32_t sb = sa + L.a_bytes;
+      // MMAs of one N half of one staged K block
+      auto issue_half = [&](uint32_t slot, int h, int kb) {
+        const uint32_t sa = smem_u32(smem + slot * L.stage_bytes);
+        const uint32_t sb = sa + L.a_bytes + h * B_BOX * GEMM_ROW_BYTES;
+        const uint32_t d = tmem_base + acc_stage * BN + h * MMA_N;
 #pragma unroll
-          for (int k = 0; k < KSTEPS; ++k) {
-            const uint64_t ad = make_sw128_desc(sa + k * UMMA_K_BYTES, 16, 1024);
-#pragma unroll
-            for (int h = 0; h < NH; ++h) {
-              const uint64_t bd = make_sw128_desc(sb + h * B_BOX * GEMM_ROW_BYTES + k * UMMA_K_BYTES, 16, 1024);
-              if constexpr (IN == IN_E4M3)
-                mma_f8_ss<CG>(d_tmem + h * MMA_N, ad, bd, IDESC, (kb | k) != 0);
-              else
-                mma_f16_ss<CG>(d_tmem + h * MMA_N, ad, bd, IDESC, (kb | k) != 0);
-            }
-          }
-          if constexpr (CG == 1)
-            ring->consumed_by_mma(c);
+        for (int k = 0; k < KSTEPS; ++k) {
+          const uint64_t ad = make_sw128_desc(sa + k * UMMA_K_BYTES, 16, 1024);
+          const uint64_t bd = make_sw128_desc(sb + k * UMMA_K_BYTES, 16, 1024);
+          if constexpr (IN == IN_E4M3)
+            mma_f8_ss<CG>(d, ad, bd, IDESC, (kb | k) != 0);
           else
-            mma_commit_mc2(&ring->empty[c.slot], 0x3);  // release the slot in both CTAs
-          c.advance(D);
+            mma_f16_ss<CG>(d, ad, bd, IDESC, (kb | k) != 0);
         }
-        // accumulator aref: put by the tensor core
+      };
+      auto release = [&](uint32_t slot) {  // aref consumed, performed by the tensor core
         if constexpr (CG == 1)
-          mma_commit(&tmem_full[acc_stage]);
+          mma_commit(&ring->empty[slot]);
         else
-          mma_commit_mc2(&tmem_full[acc_stage], 0x3);
-        if (++acc_stage == ACC) {
-          acc_stage = 0;
+          mma_commit_mc2(&ring->empty[slot], 0x3);  // release the slot in both CTAs
+      };
+      auto commit_full = [&](int i) {  // accumulator aref: put by the tensor core
+        if constexpr (CG == 1)
+          mma_commit(&tmem_full[i]);
+        else
+          mma_commit_mc2(&tmem_full[i], 0x3);
+      };
+      if (NH == 2 && P == D) {
+        // 256 x 512 tiles, one TMEM accumulator handed over half by half: the last D-1 K blocks
+        // of a tile issue their half-0 MMAs first (half 1 deferred, its stages held), so half 0
+        // completes early and its epilogue drains while the tensor core finishes half 1; the next
+        // tile starts on half 0 as soon as that is drained and defers half 1 (up to D-1 K blocks)
+        // until the epilogue has released it. The tensor core never waits for a whole epilogue.
+        uint32_t pend_slot[GEMM_MAX_STAGES];
+        int pend_kb[GEMM_MAX_STAGES];
+        for (int t = tile0; t < num_tiles; t += tile_stride) {
+          const uint32_t par = acc_phase ^ 1u;
+          mbar_wait(&tmem_empty[0], par, 3);
+          tc_fence_after();
+          bool h1_free = false;
+          int npend = 0;
+          auto flush = [&]() {
+            for (int i = 0; i < npend; ++i) {
+              issue_half(pend_slot[i], 1, pend_kb[i]);
+              release(pend_slot[i]);
+            }
+            npend = 0;
+          };
+          const int nk = p.num_k_blocks, tail = nk - static_cast<int>(D) + 1;
+          for (int kb = 0; kb < nk; ++kb) {
+            ring->get(c, 2);
+            tc_fence_after();
+            issue_half(c.slot, 0, kb);
+            if (!h1_free && mbar_try_wait(smem_u32(&tmem_empty[1]), par)) {
+              h1_free = true;
+              tc_fence_after();
+            }
+            if ((!h1_free || kb >= tail) && npend < static_cast<int>(D) - 1) {
+              pend_slot[npend] = c.slot;
+              pend_kb[npend++] = kb;
+            } else {
+              if (!h1_free) {
+                mbar_wait(&tmem_empty[1], par, 3);
+                tc_fence_after();
+                h1_free = true;
+              }
+              flush();
+              issue_half(c.slot, 1, kb);
+              release(c.slot);
+            }
+            c.advance(D);
+          }
+          commit_full(0);
+          if (!h1_free) {
+            mbar_wait(&tmem_empty[1], par, 3);
+            tc_fence_after();
+          }
+          flush();
+          commit_full(1);
           acc_phase ^= 1u;
+        }
+      } else {
+        for (int t = tile0; t < num_tiles; t += tile_stride) {
+          mbar_wait(&tmem_empty[acc_stage], acc_phase ^ 1u, 3);
+          if (NH == 2) mbar_wait(&tmem_empty[1], acc_phase ^ 1u, 3);
+          tc_fence_after();
+          for (int kb = 0; kb < p.num_k_blocks; ++kb, ++gk) {
+            if (P < D && gk >= P) {
+              // at most P k-blocks of MMAs in flight (ref pipeline.hpp:98-140, "wait <= P-1")
+              const uint32_t old = gk - P;
+              mbar_wait(&ring->empty[old % D], (old / D) & 1u, 4);
+            }
+            ring->get(c, 2);
+            tc_fence_after();
+#pragma unroll
+            for (int h = 0; h < NH; ++h) issue_half(c.slot, h, kb);
+            release(c.slot);
+            c.advance(D);
+          }
+          commit_full(acc_stage);
+          if (NH == 2) commit_full(1);
+          if (++acc_stage == ACC) {
+            acc_stage = 0;
+            acc_phase ^= 1u;
+          }
         }
       }
     }
@@ -236,7 +303,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       int mb, nb;
       gemm_tile_coords(t, p, p.num_m_blocks / CG, mb, nb);
       const int crow = mb * GEMM_BM * CG + static_cast<int>(rank) * GEMM_BM;
-      mbar_wait(&tmem_full[acc_stage], acc_phase, 5);
+      // BN = 512: this warp's column half is one N half with its own barrier pair
+      const int bar = NH == 2 ? hc : static_cast<int>(acc_stage);
+      mbar_wait(&tmem_full[bar], acc_phase, 5);
       tc_fence_after();
       const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc_stage * BN + hc * (BN / 2);
       // one chunk: CW columns = 128 bytes of output per row
@@ -250,9 +319,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           __syncwarp();
           if (lane == 0) {
             if constexpr (CG == 1)
-              mbar_arrive(&tmem_empty[acc_stage]);
+              mbar_arrive(&tmem_empty[bar]);
             else
-              mbar_arrive_cluster(&tmem_empty[acc_stage], 0);  // the leader's MMA warp owns the release
+              mbar_arrive_cluster(&tmem_empty[bar], 0);  // the leader's MMA warp owns the release
           }
         }
         uint32_t w[32];

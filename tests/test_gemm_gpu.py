@@ -116,15 +116,18 @@ def test_n_column_shards_cover_the_output(ws, dev, world):
     assert np.array_equal(as_f64(c), _want(M, N, K))
 
 
-@pytest.mark.parametrize("K", [256, 8192])
-def test_full_size_8192_sampled_rows_exact(ws, dev, K):
+@pytest.mark.parametrize("K,kw", [(256, {}), (8192, {}), (64, dict(cta_pair=True, bn=512)),
+                                  (192, dict(cta_pair=True, bn=512)), (1024, dict(cta_pair=True, bn=512))])
+def test_full_size_8192_sampled_rows_exact(ws, dev, K, kw):
     """C2 at full size: every row checked for the size-independent row-sum identity
     sum_n c[m,n] = a[m,:] . (sum_n b[n,:]), and 24 sampled rows (first/last of tiles and groups)
-    bit-exact against the oracle."""
+    bit-exact against the oracle. The 256x512 cases run ~7 tiles per CTA pair with 1, 3 and 16 K
+    blocks: the half-by-half accumulator hand-over with head deferral (fewer K blocks than stages),
+    tail deferral and both."""
     M = N = 8192
     a = ref_tensor("a", (M, K), BF16, dev)
     b = ref_tensor("b", (N, K), BF16, dev)
-    c = ws.gemm_tn(a, b, out_dtype=F32)
+    c = ws.gemm_tn(a, b, out_dtype=F32, **kw)
     torch.cuda.synchronize()
     rowsum = c.double().sum(1)
     want_rowsum = a.double() @ b.double().sum(0)
