@@ -318,6 +318,7 @@ def run_ours(args):
 
     # ---- attention path (C4 / C5), reported beside the headline ----
     attn = bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier)
+    other_configs = bench_fp8_and_c1(ws, torch, dev, stream, args, world, max_over_ranks, barrier)
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the timed region ----
     e2e = bench_e2e(ws, torch, dev, stream, args, world, max_over_ranks, barrier)
@@ -333,6 +334,7 @@ def run_ours(args):
         "tflops_per_k": per_k,
         "gemm_8192_cubed_tflops": per_k["8192"],
         "attention": attn,
+        "other_configs": other_configs,
         "roofline": roofline,
         "e2e": e2e,
         "gpu_launches": launches,
@@ -353,10 +355,14 @@ def run_ours(args):
 
 def bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier):
     out = {}
+    # C4: non-causal hdim 128, 16 heads, S 1K..16K with B*S = 16K; C5: causal S = 16K, hdim 64/128
     cases = [("c4_noncausal_s16k_d128", 1, 16, 16384, 128, False),
+             ("c4_noncausal_s8k_d128_b2", 2, 16, 8192, 128, False),
+             ("c4_noncausal_s4k_d128_b4", 4, 16, 4096, 128, False),
+             ("c4_noncausal_s2k_d128_b8", 8, 16, 2048, 128, False),
+             ("c4_noncausal_s1k_d128_b16", 16, 16, 1024, 128, False),
              ("c5_causal_s16k_d128", 1, 16, 16384, 128, True),
-             ("c5_causal_s16k_d64", 1, 16, 16384, 64, True),
-             ("c4_noncausal_s1k_d128_b16", 16, 16, 1024, 128, False)]
+             ("c5_causal_s16k_d64", 1, 16, 16384, 64, True)]
     iters = max(3, min(args.steps, 20))
     for name, B, H, S, Dh, causal in cases:
         q = torch.randn(B, H, S, Dh, device=dev, dtype=torch.bfloat16)
@@ -376,10 +382,46 @@ def bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier
         torch.cuda.synchronize()
         ms = max_over_ranks(e0.elapsed_time(e1) / iters)
         fl = 4.0 * B * H * S * S * Dh / (2 if causal else 1)
-        out[name] = {"tflops": round(world * fl / (ms * 1e-3) / 1e12, 1), "ms": round(ms, 4),
-                     "frac_of_peak": round(fl / (ms * 1e-3) / 1e12 / load_peaks()["bf16_sustained"], 4)}
+        tf = fl / (ms * 1e-3) / 1e12
+        out[name] = {"tflops": round(world * tf, 1), "ms": round(ms, 4),
+                     "frac_of_measured_sustained_bf16": round(tf / load_peaks()["bf16_sustained"], 4),
+                     "frac_of_dense_2250": round(tf / 2250.0, 4)}
         del q, k, v, o, lse
     return out
+
+
+def bench_fp8_and_c1(ws, torch, dev, stream, args, world, max_over_ranks, barrier):
+    """C3 (FP8 e4m3 GEMM M=N=8192, K sweep, fp32 accumulate, per-tensor scales, bf16 out) and C1
+    (fp16 1024^3, fp32 out), device time per launch, reported beside the headline."""
+    res = {"c3_fp8_tflops_per_k": {}}
+    iters = max(3, min(args.steps, 20))
+
+    def timed(fn):
+        for _ in range(3):
+            fn()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            fn()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return max_over_ranks(e0.elapsed_time(e1) / iters)
+
+    c = torch.empty(M_, N_, device=dev, dtype=torch.bfloat16)
+    for K in K_SWEEP:
+        a = (torch.randn(M_, K, device=dev) * 0.5).to(torch.float8_e4m3fn)
+        b = (torch.randn(N_, K, device=dev) * 0.5).to(torch.float8_e4m3fn)
+        ms = timed(lambda: ws.gemm_tn(a, b, c, scale_a=0.5, scale_b=2.0))
+        res["c3_fp8_tflops_per_k"][str(K)] = round(world * gemm_flops(K) / (ms * 1e-3) / 1e12, 1)
+        del a, b
+    a = torch.randn(1024, 1024, device=dev).half()
+    b = torch.randn(1024, 1024, device=dev).half()
+    c1 = torch.empty(1024, 1024, device=dev, dtype=torch.float32)
+    ms = timed(lambda: ws.gemm_tn(a, b, c1))
+    res["c1_fp16_1024_cubed_tflops"] = round(world * 2 * 1024 ** 3 / (ms * 1e-3) / 1e12, 1)
+    return res
 
 
 def bench_e2e(ws, torch, dev, stream, args, world, max_over_ranks, barrier):
