@@ -315,6 +315,12 @@ def run_ours(args):
                 "frac_of_burst": round(achieved / peaks["bf16"], 4),
                 "frac_of_dense_2250": round(achieved / 2250.0, 4),
                 "share_of_step": round(dom_ms / ms_per_step, 3)}
+    # the GPU is power-capped under sustained tensor load, so also state the dense bf16 peak at the
+    # SM clock sampled during the timed region (148 SMs x 8192 FLOP/clk): the per-clock efficiency
+    if clocks.get("sm_mhz"):
+        clk_peak = 148 * 8192 * clocks["sm_mhz"] * 1e6 / 1e12
+        roofline["peak_at_sampled_clock"] = round(clk_peak, 1)
+        roofline["frac_at_sampled_clock"] = round(achieved / clk_peak, 4)
 
     # ---- attention path (C4 / C5), reported beside the headline ----
     attn = bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier)
