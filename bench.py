@@ -393,6 +393,28 @@ def bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier
                      "frac_of_measured_sustained_bf16": round(tf / load_peaks()["bf16_sustained"], 4),
                      "frac_of_dense_2250": round(tf / 2250.0, 4)}
         del q, k, v, o, lse
+    # FP8 e4m3 attention (hdim 128, per-tensor descales, bf16 O)
+    for name, causal in (("fp8_noncausal_s16k_d128", False), ("fp8_causal_s16k_d128", True)):
+        q = torch.randn(1, 16, 16384, 128, device=dev).to(torch.float8_e4m3fn)
+        k = torch.randn(1, 16, 16384, 128, device=dev).to(torch.float8_e4m3fn)
+        v = torch.randn(1, 16, 16384, 128, device=dev).to(torch.float8_e4m3fn)
+        o = torch.empty(1, 16, 16384, 128, device=dev, dtype=torch.bfloat16)
+        lse = torch.empty(1, 16, 16384, device=dev)
+        for _ in range(3):
+            ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse)
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(iters):
+            ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms = max_over_ranks(e0.elapsed_time(e1) / iters)
+        fl = 4.0 * 16 * 16384 * 16384 * 128 / (2 if causal else 1)
+        out[name] = {"tflops": round(world * fl / (ms * 1e-3) / 1e12, 1), "ms": round(ms, 4),
+                     "frac_of_dense_fp8_4500": round(fl / (ms * 1e-3) / 1e12 / 4500.0, 4)}
+        del q, k, v, o, lse
     return out
 
 

@@ -87,7 +87,8 @@ typedef struct ws_gemm_desc {
 
 /* FlashAttention forward. q,k,v,o: [B, H, S, Dh] contiguous; lse: [B, H, S] fp32 (natural log,
  * lse = m + log(l)); may be NULL. Only bh in [bh_begin, bh_end) is computed (the multi-GPU
- * batch*heads shard); bh_end <= 0 means B*H. dtype in {BF16, F16}; Dh in {64, 128};
+ * batch*heads shard); bh_end <= 0 means B*H. dtype in {BF16, F16, E4M3 (Dh 128; o is BF16;
+ * P is quantized to e4m3 for the P.V product)}; Dh in {64, 128};
  * S % 128 == 0. softmax_scale <= 0 means 1/sqrt(Dh). */
 typedef struct ws_attn_desc {
   int32_t dtype;
@@ -102,6 +103,8 @@ typedef struct ws_attn_desc {
   int32_t kv_block;            /* keys per K/V block: 0 = auto (128), 64 or 128. 128-key blocks
                                   keep the QK^T MMA inside the shared-memory operand rate; 64
                                   double-buffers S per Q tile instead (csrc/attn*_sm100.cuh) */
+  float scale_q, scale_k, scale_v; /* E4M3 only: per-tensor descales (0 = 1): scores use
+                                  scale_q*scale_k*q.k, O = scale_v * P.v / l */
 } ws_attn_desc;
 
 ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream);

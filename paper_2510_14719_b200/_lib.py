@@ -48,6 +48,7 @@ class AttnDesc(ctypes.Structure):
         ("D", ctypes.c_int32),
         ("bh_begin", ctypes.c_int32), ("bh_end", ctypes.c_int32),
         ("kv_block", ctypes.c_int32),
+        ("scale_q", ctypes.c_float), ("scale_k", ctypes.c_float), ("scale_v", ctypes.c_float),
     ]
 
 

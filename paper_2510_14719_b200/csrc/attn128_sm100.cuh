@@ -42,7 +42,8 @@ struct Attn128Params {
   int causal;
   int bh_fast;        // grid order: 1 = blockIdx.x walks (b,h) (causal, heaviest pairs first);
                       // 0 = blockIdx.x walks the query pairs of one (b,h) (K/V stay L2-resident)
-  float scale_log2;   // softmax_scale * log2(e)
+  float scale_log2;   // softmax_scale * log2(e) (* q, k descales for FP8)
+  float o_scale;      // V descale folded into the epilogue (1 unless FP8)
   float* lse;
   void* o;
   unsigned long long* trace;  // optional %clock64 stamps of CTA (0,0), layout of attn_sm100.cuh

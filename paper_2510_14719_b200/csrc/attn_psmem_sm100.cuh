@@ -48,16 +48,20 @@ __host__ __device__ inline uint32_t aps_smem_bytes(int Dh, int kv_stages) {
          (2 * A128_MAX_STAGES + 16) * 8 + 16 + 1024;
 }
 
-template <int DH, bool BF16, int POLY = 2, bool TRACE = false>
+// FP8: Q, K, V in e4m3 (kind::f8f6f4 QK and PV, P quantized to e4m3 in shared memory, per-tensor
+// descales folded into the softmax scale and the epilogue), O in bf16.
+template <int DH, bool BF16, int POLY = 2, bool TRACE = false, bool FP8 = false>
 __global__ void __launch_bounds__(A128_THREADS, 1)
     ws_attn_psmem_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const Attn128Params p) {
-  constexpr uint32_t QTILE = A128_BM * DH * 2;       // bytes of a 128 x DH Q tile
-  constexpr uint32_t PTILE = A128_BM * A128_BN * 2;  // bytes of a 128 x 128 P tile
-  constexpr uint32_t KVTILE = A128_BN * DH * 2;      // bytes of a 128 x DH K or V block
+  constexpr int EB = FP8 ? 1 : 2;                     // operand element bytes
+  constexpr uint32_t QTILE = A128_BM * DH * EB;       // bytes of a 128 x DH Q tile
+  constexpr uint32_t PTILE = A128_BM * A128_BN * EB;  // bytes of a 128 x 128 P tile
+  constexpr uint32_t KVTILE = A128_BN * DH * EB;      // bytes of a 128 x DH K or V block
   constexpr uint32_t PANEL = 128 * 128;              // one 64-column (128 B) swizzle panel of 128 rows
-  constexpr int NPANEL = DH / 64;
-  constexpr uint32_t FMT = BF16 ? 1u : 0u;
+  constexpr int NPANEL = DH * EB / 128;               // 128-byte panels per Q / K / V row
+  constexpr int PANEL_ELEMS = 128 / EB;
+  constexpr uint32_t FMT = FP8 ? 0u : BF16 ? 1u : 0u;   // kind::f8f6f4 e4m3 / kind::f16 bf16, f16
   constexpr uint32_t IDESC_QK = make_idesc(FMT, A128_BM, A128_BN, 0, 0);
   constexpr uint32_t IDESC_PV = make_idesc(FMT, A128_BM, DH, 0, 1);  // A = P K-major, B = V MN-major
   constexpr uint32_t COL_O = 2 * A128_BN;
@@ -154,14 +158,14 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         for (int t = 0; t < 2; ++t)
 #pragma unroll
           for (int h = 0; h < NPANEL; ++h)
-            tma_load_2d(sq + t * QTILE + h * PANEL, &tm_q, q_full, h * 64, q_row0 + t * A128_BM);
+            tma_load_2d(sq + t * QTILE + h * PANEL, &tm_q, q_full, h * PANEL_ELEMS, q_row0 + t * A128_BM);
         auto put = [&](const CUtensorMap* m, int blk) {
           ring->put_acquire(c, 10);
           ring->put_expect(c, KVTILE);
           uint8_t* dst = skv + c.slot * KVTILE;
 #pragma unroll
           for (int h = 0; h < NPANEL; ++h)
-            tma_load_2d(dst + h * PANEL, m, &ring->full[c.slot], h * 64, kv_row0 + blk * A128_BN);
+            tma_load_2d(dst + h * PANEL, m, &ring->full[c.slot], h * PANEL_ELEMS, kv_row0 + blk * A128_BN);
           c.advance(D);
         };
         // ring order = MMA consumption order: K_0, then (K_{j+1}, V_j) for j = 0 .. n1-1
@@ -182,19 +186,28 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     auto issue_qk = [&](int t, uint32_t k_slot) {
       const uint64_t a0 = qdesc + ((t * QTILE) >> 4), b0 = kdesc + ((k_slot * KVTILE) >> 4);
 #pragma unroll
-      for (int k = 0; k < DH / 16; ++k) {
+      for (int k = 0; k < DH * EB / 32; ++k) {  // one MMA per 32 bytes of the head dim
         const uint32_t off = ((k / 4) * PANEL + (k % 4) * 32) >> 4;
-        mma_f16_ss_warp(tmem + t * A128_BN, a0 + off, b0 + off, IDESC_QK, k != 0);
+        if constexpr (FP8)
+          mma_f8_ss_warp(tmem + t * A128_BN, a0 + off, b0 + off, IDESC_QK, k != 0);
+        else
+          mma_f16_ss_warp(tmem + t * A128_BN, a0 + off, b0 + off, IDESC_QK, k != 0);
       }
     };
     auto issue_pv = [&](int t, uint32_t v_slot, bool acc) {
       const uint64_t a0 = pdesc + ((t * PTILE) >> 4), b0 = vdesc + ((v_slot * KVTILE) >> 4);
+      constexpr int KEYS = 32 / EB;  // keys per MMA (32 bytes of P)
 #pragma unroll
-      for (int k = 0; k < A128_BN / 16; ++k) {
-        // A = P_t keys [16k, 16k+16) (K-major panel k/4); B = V rows [16k, 16k+16) (two 8-row groups)
+      for (int k = 0; k < A128_BN / KEYS; ++k) {
+        // A = P_t keys [KEYS k, KEYS (k+1)) (K-major, panel k/4); B = V rows of those keys
+        // (MN-major, KEYS/8 eight-row core groups of 128 bytes)
         const uint32_t aoff = ((k / 4) * PANEL + (k % 4) * 32) >> 4;
-        mma_f16_ss_warp(tmem + COL_O + t * DH, a0 + aoff, b0 + ((k * 16 * 128) >> 4), IDESC_PV,
-                        (acc || k != 0) ? 1u : 0u);
+        if constexpr (FP8)
+          mma_f8_ss_warp(tmem + COL_O + t * DH, a0 + aoff, b0 + ((k * KEYS * 128) >> 4), IDESC_PV,
+                         (acc || k != 0) ? 1u : 0u);
+        else
+          mma_f16_ss_warp(tmem + COL_O + t * DH, a0 + aoff, b0 + ((k * KEYS * 128) >> 4), IDESC_PV,
+                          (acc || k != 0) ? 1u : 0u);
       }
     };
     ArefCursor c;
@@ -372,12 +385,13 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       // 128B-swizzled K-major P tile as it is produced, so the shared-memory writes overlap the math
       const uint64_t sl2x2 = f2_pack(sl2, sl2), negm2 = f2_pack(-m_used, -m_used);
       uint64_t sum4[4] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
+      constexpr int KPC = 16 / EB;  // keys per 16-byte chunk of the P row
 #pragma unroll
-      for (int ch = 0; ch < A128_BN / 8; ++ch) {
-        uint32_t pk[4];
+      for (int ch = 0; ch < A128_BN / KPC; ++ch) {
+        float pf[KPC];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int c = ch * 8 + 2 * e;
+        for (int e = 0; e < KPC / 2; ++e) {
+          const int c = ch * KPC + 2 * e;
           const uint64_t x2 = f2_fma(f2_pack(s[c], s[c + 1]), sl2x2, negm2);
           uint64_t p2;
           if (attn_poly_pair(POLY, (c / 2) & 7)) {
@@ -387,12 +401,18 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
             f2_unpack(x2, x0, x1);
             p2 = f2_pack(ex2_approx(x0), ex2_approx(x1));
           }
-          sum4[e] = f2_add(sum4[e], p2);
-          float p0, p1;
-          f2_unpack(p2, p0, p1);
-          pk[e] = BF16 ? pack_bf16(p0, p1) : pack_f16(p0, p1);
+          sum4[e & 3] = f2_add(sum4[e & 3], p2);
+          f2_unpack(p2, pf[2 * e], pf[2 * e + 1]);
         }
-        // 16-byte chunk ch = keys [8ch, 8ch+8): panel ch/8, swizzled position (ch%8) ^ (row%8)
+        uint32_t pk[4];
+#pragma unroll
+        for (int w = 0; w < 4; ++w) {
+          if constexpr (FP8)
+            pk[w] = pack_e4m3x4(pf[4 * w], pf[4 * w + 1], pf[4 * w + 2], pf[4 * w + 3]);
+          else
+            pk[w] = BF16 ? pack_bf16(pf[2 * w], pf[2 * w + 1]) : pack_f16(pf[2 * w], pf[2 * w + 1]);
+        }
+        // 16-byte chunk ch = keys [KPC ch, KPC (ch+1)): panel ch/8, swizzled position (ch%8) ^ (row%8)
         const uint32_t addr = p_row + (ch / 8) * PANEL + ((static_cast<uint32_t>(ch & 7) ^ swz) << 4);
         st_shared_v4(addr, pk[0], pk[1], pk[2], pk[3]);
       }
@@ -421,7 +441,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&o_free[t]);
-    const float inv_l = 1.f / l;
+    const float inv_l = p.o_scale / l;  // V's per-tensor descale (FP8) folded into 1 / l
     const size_t grow = static_cast<size_t>(q_row0 + t * A128_BM + row);
     uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) + grow * DH * 2;
 #pragma unroll
@@ -430,7 +450,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const float a = __uint_as_float(ov[c0 + 2 * e]) * inv_l, b = __uint_as_float(ov[c0 + 2 * e + 1]) * inv_l;
-        w[e] = BF16 ? pack_bf16(a, b) : pack_f16(a, b);
+        w[e] = (BF16 || FP8) ? pack_bf16(a, b) : pack_f16(a, b);
       }
       *reinterpret_cast<uint4*>(orow + c0 * 2) = make_uint4(w[0], w[1], w[2], w[3]);
     }

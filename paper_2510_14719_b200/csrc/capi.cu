@@ -282,6 +282,7 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
   p.bh_fast = d.causal ? 1 : 0;
   const float sm = d.softmax_scale > 0.f ? d.softmax_scale : 1.0f / std::sqrt((float)DH);
   p.scale_log2 = sm * 1.4426950408889634f;
+  p.o_scale = 1.f;
   p.lse = d.LSE;
   p.o = d.O;
   p.trace = trace;
@@ -339,8 +340,63 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
   return WS_OK;
 }
 
+// FP8 e4m3 attention (hdim 128): the P-in-shared-memory kernel with kind::f8f6f4 MMAs, P
+// quantized to e4m3, per-tensor descales (q, k into the softmax scale, v into the epilogue), bf16 O.
+ws_status launch_attn_fp8(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stream, unsigned long long* trace) {
+  using namespace ws;
+  constexpr int DH = 128;
+  const int64_t rows = (int64_t)d.B * d.H * d.S;
+  Attn128Params p;
+  p.S = d.S;
+  p.BH_begin = bh0;
+  p.num_pairs = d.S / (2 * A128_BM);
+  p.num_bh = bh1 - bh0;
+  p.stagger = 1;
+  p.causal = d.causal;
+  p.bh_fast = d.causal ? 1 : 0;
+  const float sq = d.scale_q > 0.f ? d.scale_q : 1.f, sk = d.scale_k > 0.f ? d.scale_k : 1.f;
+  const float sv = d.scale_v > 0.f ? d.scale_v : 1.f;
+  const float sm = d.softmax_scale > 0.f ? d.softmax_scale : 1.0f / std::sqrt((float)DH);
+  p.scale_log2 = sm * sq * sk * 1.4426950408889634f;
+  p.o_scale = sv;
+  p.lse = d.LSE;
+  p.o = d.O;
+  p.trace = trace;
+  const uint32_t kvb = A128_BN * DH;  // one e4m3 K or V block
+  const uint32_t base = 2 * A128_BM * DH + 2 * A128_BM * A128_BN + (2 * A128_MAX_STAGES + 16) * 8 + 16 + 1024;
+  int max_stages = (SMEM_LIMIT - (int)base) / (int)kvb;
+  if (max_stages > A128_MAX_STAGES) max_stages = A128_MAX_STAGES;
+  p.kv_stages = d.D > 0 ? d.D : max_stages;
+  if (p.kv_stages < 2)
+    return fail(WS_PIPELINE_INFEASIBLE, "the K/V aref needs D >= 2 (ref pipeline.hpp:309-315)");
+  const uint32_t smem = base + p.kv_stages * kvb;
+  if (p.kv_stages > A128_MAX_STAGES || (int)smem > SMEM_LIMIT)
+    return fail(WS_SMEM_OVERFLOW, "D=" + std::to_string(p.kv_stages) + " K/V stages need " + std::to_string(smem) +
+                                      " B of shared memory; limit " + std::to_string(SMEM_LIMIT));
+  CUtensorMap tq, tk, tv;
+  ws_status s;
+  if ((s = make_tmap(&tq, d.Q, WS_E4M3, rows, DH, DH, A128_BM, 128, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
+    return s;
+  if ((s = make_tmap(&tk, d.K, WS_E4M3, rows, DH, DH, A128_BN, 128, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
+    return s;
+  if ((s = make_tmap(&tv, d.V, WS_E4M3, rows, DH, DH, A128_BN, 128, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
+    return s;
+  auto kern = trace ? ws_attn_psmem_kernel<DH, true, APS_POLY, true, true> : ws_attn_psmem_kernel<DH, true, APS_POLY, false, true>;
+  WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  cudaLaunchConfig_t cfg = {};
+  const int items = p.num_pairs * p.num_bh;
+  cfg.gridDim = dim3(items < num_sms() ? items : num_sms());
+  cfg.blockDim = dim3(A128_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, p));
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return WS_OK;
+}
+
 ws_status attn_entry(const ws_attn_desc& d, cudaStream_t st, unsigned long long* trace) {
-  if (d.dtype != WS_BF16 && d.dtype != WS_F16) return fail(WS_TYPE, "attention dtype must be BF16 or F16");
+  if (d.dtype != WS_BF16 && d.dtype != WS_F16 && d.dtype != WS_E4M3)
+    return fail(WS_TYPE, "attention dtype must be BF16, F16 or E4M3");
   if (d.B <= 0 || d.H <= 0 || d.S <= 0) return fail(WS_TYPE, "B, H, S must be positive");
   if (d.Dh != 64 && d.Dh != 128) return fail(WS_UNSUPPORTED_KERNEL, "head dim must be 64 or 128");
   if (d.S % 256) return fail(WS_INDIVISIBLE_TILE, "S=" + std::to_string(d.S) + " is not a multiple of 256");
@@ -353,6 +409,11 @@ ws_status attn_entry(const ws_attn_desc& d, cudaStream_t st, unsigned long long*
   if ((int64_t)BH * d.S >= (int64_t)1 << 31) return fail(WS_TYPE, "B*H*S must fit in int32");
   if (d.kv_block != 0 && d.kv_block != 64 && d.kv_block != 128)
     return fail(WS_TYPE, "kv_block must be 0 (auto), 64 or 128");
+  if (d.dtype == WS_E4M3) {
+    if (d.Dh != 128) return fail(WS_UNSUPPORTED_KERNEL, "FP8 attention supports head dim 128");
+    if (d.kv_block == 64) return fail(WS_UNSUPPORTED_KERNEL, "FP8 attention uses 128-key K/V blocks");
+    return launch_attn_fp8(d, bh0, bh1, st, trace);
+  }
   if (d.kv_block != 64) {
     // P staging: hdim 128 stages P in shared memory (S released early, QK_{j+1} overlaps the
     // softmax); hdim 64 keeps P in TMEM (its shared-memory P tiles would leave less room for the

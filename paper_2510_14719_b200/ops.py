@@ -78,22 +78,23 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool 
              softmax_scale: Optional[float] = None, out: Optional[torch.Tensor] = None,
              lse: Optional[torch.Tensor] = None, D: int = 0, bh_range: Optional[tuple] = None,
              stream: Optional[torch.cuda.Stream] = None, trace: Optional[torch.Tensor] = None,
-             kv_block: int = 0):
+             kv_block: int = 0, scale_q: float = 1.0, scale_k: float = 1.0, scale_v: float = 1.0):
     """FlashAttention forward over [B, H, S, Dh] tensors. Returns (o, lse) with lse fp32 [B, H, S]
     in natural-log units (lse = m + log l of the .k's running max m and row sum l).
 
     trace: optional int64 CUDA tensor of 3*256*8 entries receiving %clock64 stamps of CTA (0,0)
-    (see ws_attn_fwd_traced in include/ws.h). kv_block: keys per K/V block (0 = auto = 128, or 64)."""
+    (see ws_attn_fwd_traced in include/ws.h). kv_block: keys per K/V block (0 = auto = 128, or 64).
+    float8_e4m3fn q/k/v (hdim 128): scale_q/k/v are the per-tensor descales; o is bf16."""
     if q.device.type != "cuda":
         raise _lib.WsError(2, "operands must be CUDA tensors (no CPU path)")
-    if not (q.dtype == k.dtype == v.dtype) or q.dtype not in (torch.float16, torch.bfloat16):
+    if not (q.dtype == k.dtype == v.dtype) or q.dtype not in (torch.float16, torch.bfloat16, torch.float8_e4m3fn):
         raise _lib.WsError(2, f"unsupported dtype {q.dtype}")
     B, H, S, Dh = q.shape
     for t in (q, k, v):
         if tuple(t.shape) != (B, H, S, Dh) or not t.is_contiguous():
             raise _lib.WsError(2, "q, k, v must be contiguous [B, H, S, Dh]")
     if out is None:
-        out = torch.empty_like(q)
+        out = torch.empty_like(q, dtype=torch.bfloat16 if q.dtype == torch.float8_e4m3fn else q.dtype)
     if lse is None:
         lse = torch.empty((B, H, S), dtype=torch.float32, device=q.device)
     d = _lib.AttnDesc()
@@ -107,6 +108,7 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool 
     lo, hi = bh_range if bh_range is not None else (0, B * H)
     d.bh_begin, d.bh_end = lo, hi
     d.kv_block = kv_block
+    d.scale_q, d.scale_k, d.scale_v = scale_q, scale_k, scale_v
     lib = _lib.load()
     if trace is not None:
         _lib.check(lib.ws_attn_fwd_traced(ctypes.byref(d), ctypes.c_void_p(_stream_ptr(stream)),

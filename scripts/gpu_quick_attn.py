@@ -79,3 +79,18 @@ if __name__ == "__main__":
             print(f"flash_attn lib S=16K causal={c}: {ms:.3f} ms {4*16*16384**2*128/(2 if c else 1)/ms/1e9:.1f} TFLOP/s")
     except Exception as e:
         print("flash_attn lib unavailable:", e)
+
+
+def bench_fp8(B, H, S, causal, iters=10):
+    q = torch.randn(B, H, S, 128, device="cuda").to(torch.float8_e4m3fn); k = torch.randn_like(q.float()).to(torch.float8_e4m3fn)
+    v = torch.randn_like(q.float()).to(torch.float8_e4m3fn)
+    o = torch.empty(B, H, S, 128, device="cuda", dtype=torch.bfloat16); lse = torch.empty(B, H, S, device="cuda")
+    for _ in range(3): ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse)
+    torch.cuda.synchronize()
+    e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(iters): ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse)
+    e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / iters
+    fl = 4 * B * H * S * S * 128 / (2 if causal else 1)
+    print(f"BENCH fp8 attn B={B} H=16 S={S} causal={causal}: {ms:.3f} ms {fl/ms/1e9:.1f} TFLOP/s", flush=True)

@@ -30,12 +30,35 @@ def test_library_exports_every_declared_symbol(ws):
     assert lib.ws_launch_count() >= 0
 
 
-def test_desc_layout_matches_header():
+def test_desc_layout_matches_header(tmp_path):
+    """The ctypes mirrors have the C structs' size and every field's offset (checked against the
+    header compiled by the host C compiler, when one is present)."""
+    import shutil
+    import subprocess
+
     from paper_2510_14719_b200 import _lib
 
     # in_dtype,out_dtype (8) + M,N,K (24) + A,lda,B,ldb,C,ldc (48) + scales (8) + 7 ints (28) -> 116, padded 120
     assert ctypes.sizeof(_lib.GemmDesc) == 120
-    assert ctypes.sizeof(_lib.AttnDesc) == 4 * 7 + 4 + 8 * 5 + 4 * 3 + 4  # padded to 8
+    cc = shutil.which("gcc") or shutil.which("cc")
+    if cc is None:
+        pytest.skip("no host C compiler")
+    lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{os.path.join(ROOT, "include", "ws.h")}"',
+             "int main(void) {"]
+    for cname, py in (("ws_gemm_desc", _lib.GemmDesc), ("ws_attn_desc", _lib.AttnDesc)):
+        lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
+        for f, _ in py._fields_:
+            lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
+    lines.append("return 0; }")
+    src = tmp_path / "layout.c"
+    src.write_text("\n".join(lines))
+    exe = tmp_path / "layout"
+    subprocess.check_call([cc, "-o", str(exe), str(src)])
+    got = dict((" ".join(l.split()[:2]), int(l.split()[2])) for l in subprocess.check_output([str(exe)], text=True).splitlines())
+    for cname, py in (("ws_gemm_desc", _lib.GemmDesc), ("ws_attn_desc", _lib.AttnDesc)):
+        assert got[f"{cname} size"] == ctypes.sizeof(py)
+        for f, _ in py._fields_:
+            assert got[f"{cname} {f}"] == getattr(py, f).offset, (cname, f)
 
 
 def _gemm_desc(ws, **kw):
@@ -88,7 +111,9 @@ def _attn_desc(ws, **kw):
     (dict(D=4), "smem-overflow"),                   # hdim 128, P in shared memory: room for 3 K/V slots
     (dict(D=9, kv_block=64), "smem-overflow"),
     (dict(kv_block=96), "type"),
-    (dict(dtype=3), "type"),
+    (dict(dtype=0), "type"),                        # fp32 attention is not a tensor-core kind here
+    (dict(dtype=3, Dh=64), "unsupported-kernel"),   # FP8 attention: hdim 128 only
+    (dict(dtype=3, kv_block=64), "unsupported-kernel"),
     (dict(bh_begin=1, bh_end=1), "type"),
 ])
 def test_attn_validation_codes(ws, kw, code):
