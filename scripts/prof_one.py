@@ -5,7 +5,7 @@ import torch
 import paper_2510_14719_b200 as ws
 
 ap = argparse.ArgumentParser()
-ap.add_argument("what", choices=["gemm", "gemm_fp8", "attn", "attn_causal", "attn_causal64"])
+ap.add_argument("what", choices=["gemm", "gemm_fp8", "attn", "attn_causal", "attn_causal64", "attn_fp8"])
 ap.add_argument("--K", type=int, default=16384)
 ap.add_argument("--n", type=int, default=3)
 ap.add_argument("--bn", type=int, default=0)
@@ -23,8 +23,10 @@ if a.what.startswith("gemm"):
         ws.gemm_tn(A, B, C, bn=a.bn, D=a.D, P=a.P, cta_pair=a.cta_pair)
 else:
     Dh = 64 if a.what == "attn_causal64" else 128
-    q = torch.randn(1, 16, 16384, Dh, device=dev, dtype=torch.bfloat16); k = torch.randn_like(q); v = torch.randn_like(q)
+    dt = torch.float8_e4m3fn if a.what == "attn_fp8" else torch.bfloat16
+    q = torch.randn(1, 16, 16384, Dh, device=dev).to(dt); k = torch.randn(1, 16, 16384, Dh, device=dev).to(dt)
+    v = torch.randn(1, 16, 16384, Dh, device=dev).to(dt)
     for _ in range(a.n):
-        ws.attn_fwd(q, k, v, causal=a.what != "attn", D=a.D, kv_block=a.kvb)
+        ws.attn_fwd(q, k, v, causal=a.what not in ("attn", "attn_fp8"), D=a.D, kv_block=a.kvb)
 torch.cuda.synchronize()
 print("done", a)
