@@ -113,6 +113,20 @@ int num_sms() {
 
 constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA on sm_100a
 
+// Suspend-time hint of blocked mbarrier waits in this module's kernels: a waiting warp sleeps in
+// the barrier (woken when the phase completes) instead of re-issuing try_wait, which leaves the
+// issue slots to the softmax warps sharing its SM sub-partition (hdim-64 causal attention +5-10%,
+// GEMM unchanged; scripts/attn_ab.py). WS_WAIT_HINT_NS overrides (0 = hardware default). Set once
+// per device context before the first launch.
+void apply_wait_hint() {
+  static std::once_flag once;
+  std::call_once(once, [] {
+    const char* e = getenv("WS_WAIT_HINT_NS");
+    const uint32_t ns = e ? static_cast<uint32_t>(atoi(e)) : 200000u;
+    cudaMemcpyToSymbol(ws::ws_wait_hint_ns, &ns, sizeof(ns));
+  });
+}
+
 template <int IN, int OUT, int BN, int CG>
 ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   using namespace ws;
@@ -175,6 +189,7 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
+  apply_wait_hint();
   WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return WS_OK;
@@ -256,6 +271,7 @@ ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stre
   cfg.blockDim = dim3(ATTN_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
+  apply_wait_hint();
   WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, p));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return WS_OK;
@@ -335,6 +351,7 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
   cfg.blockDim = dim3(A128_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
+  apply_wait_hint();
   WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, p));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return WS_OK;
@@ -389,6 +406,7 @@ ws_status launch_attn_fp8(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t 
   cfg.blockDim = dim3(A128_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
+  apply_wait_hint();
   WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, p));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return WS_OK;

@@ -27,13 +27,16 @@
 namespace ws {
 
 static __device__ WatchdogRecord ws_watchdog_record;
+// suspend-time hint (ns) for blocked waits; 0 = the hardware default (set by the host launcher)
+static __device__ uint32_t ws_wait_hint_ns;
 
 // Out of line on purpose would force ABI register saves in the 224-register softmax regions
 // (setmaxnreg budgets are per region); the slow path is inlined and stays cold.
 static __device__ __forceinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity, uint32_t tag) {
   uint64_t t0 = globaltimer();
   uint32_t spins = 0;
-  while (!mbar_try_wait(bar, parity)) {
+  const uint32_t hint = ws_wait_hint_ns;
+  while (!(hint ? mbar_try_wait_hint(bar, parity, hint) : mbar_try_wait(bar, parity))) {
     if (((++spins) & 1023u) == 0 && globaltimer() - t0 > WS_WATCHDOG_NS) {
       ws_watchdog_record.block = blockIdx.x | (static_cast<unsigned long long>(blockIdx.y) << 32);
       ws_watchdog_record.thread = threadIdx.x;
