@@ -94,9 +94,11 @@ def test_softmax_rows_sum_to_one(ws, dev, kv_block):
         assert (o.float() - 1).abs().max().item() <= 1e-2
 
 
-def test_bh_shards_cover_the_output(ws, dev):
-    """rank g computes (b,h) slices [bh_lo, bh_hi); shards tile the full result."""
-    B, H, S, Dh = 2, 4, 512, 64
+@pytest.mark.parametrize("Dh", [64, 128])
+def test_bh_shards_cover_the_output(ws, dev, Dh):
+    """rank g computes (b,h) slices [bh_lo, bh_hi); shards tile the full result (hdim 128
+    runs the persistent kernel, whose work items are offset by bh_begin)."""
+    B, H, S = 2, 4, 512
     q, k, v = _inputs(B, H, S, Dh, BF16, dev)
     full_o, full_l = ws.attn_fwd(q, k, v, causal=True)
     o = torch.full_like(q, float("nan"))
