@@ -22,6 +22,11 @@
 //   * Causal: the 256 query rows of a CTA are two 128-row tiles aligned to 128-key blocks, so the
 //     diagonal block of each tile is square and is the only block that needs a mask; tile 0 stops
 //     one block before tile 1.
+//   * Persistent (ref proj/include/warpspec/grid.hpp:93-123): grid = min(#SMs, items), CTA b runs
+//     the items of its static schedule (stride, or a snake for causal), barrier phases carry over
+//     (running block counters), and q_free / o_free hand the Q tiles and the O accumulators over to
+//     the next item. S_t needs no hand-over: the next item's QK_t(0) is issued after this item's
+//     last PV_t(j) by the same thread, and tcgen05 MMAs execute in issue order.
 #pragma once
 
 #include "attn_sm100.cuh"  // ATTN_RESCALE_THRESHOLD, attn_poly_pair, trace layout
@@ -88,31 +93,37 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
   uint64_t* q_full = reinterpret_cast<uint64_t*>(bar_base + 2 * A128_MAX_STAGES * 8);
   uint64_t* s_full = q_full + 1;  // [2]: QK_t(j) complete (and with it PV_t(j-1))
   uint64_t* p_full = q_full + 3;  // [2]: P_t(j) in S_t, O_t rescaled
-  uint64_t* o_full = q_full + 5;  // [2]: last PV_t complete
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 7);
+  uint64_t* o_full = q_full + 5;  // [2]: last PV_t of the item complete
+  uint64_t* o_free = q_full + 7;  // [2]: O_t of the item copied out by the epilogue
+  uint64_t* q_free = q_full + 9;  // the item's last QK complete: Q smem reusable
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 10);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
   const uint32_t D = static_cast<uint32_t>(p.kv_stages);
 
-  int pair, bh;
-  if (p.bh_fast) {
-    pair = p.num_pairs - 1 - static_cast<int>(blockIdx.y);
-    bh = p.BH_begin + static_cast<int>(blockIdx.x);
-  } else {
-    pair = static_cast<int>(blockIdx.x);
-    bh = p.BH_begin + static_cast<int>(blockIdx.y);
-  }
-  const int q_row0 = bh * p.S + pair * 2 * A128_BM;  // row in the [B*H*S, Dh] view
+  const int nbh = p.num_bh;
+  auto item_coords = [&](int i, int& pair, int& bh) {
+    if (p.bh_fast) {  // causal: (b,h) fastest from the heaviest query pairs down
+      pair = p.num_pairs - 1 - i / nbh;
+      bh = p.BH_begin + i % nbh;
+    } else {  // the query pairs of one (b,h) together: its K/V stay in L2
+      pair = i % p.num_pairs;
+      bh = p.BH_begin + i / p.num_pairs;
+    }
+  };
   // K/V blocks per tile: causal tile t of pair i sees blocks 0 .. 2i+t (its diagonal block last)
-  const int n0 = p.causal ? 2 * pair + 1 : p.S / A128_BN;
-  const int n1 = p.causal ? 2 * pair + 2 : p.S / A128_BN;
+  auto nblk = [&](int pair, int t) { return p.causal ? 2 * pair + 1 + t : p.S / A128_BN; };
+  const int num_items = p.num_pairs * nbh;
+  const int G = static_cast<int>(gridDim.x), b_id = static_cast<int>(blockIdx.x);
+  auto item_of = [&](int r) { return r * G + ((p.causal && (r & 1)) ? G - 1 - b_id : b_id); };
   // the traced instantiation (ws_attn_fwd_traced) is the only one carrying the stamps
   unsigned long long* const trace =
-      (TRACE && p.trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0) ? p.trace : nullptr;
+      (TRACE && p.trace != nullptr && blockIdx.x == 0) ? p.trace : nullptr;
+  // stamps of the first item of CTA 0 only
 #define WS_TRACE(role, j, ev)                                                        \
   do {                                                                              \
-    if (TRACE && trace != nullptr && (j) < ATTN_TRACE_STEPS)                        \
+    if (TRACE && trace != nullptr && it == 0 && (j) < ATTN_TRACE_STEPS)             \
       trace[((role) * ATTN_TRACE_STEPS + (j)) * 8 + (ev)] = clk64();                \
   } while (0)
 
@@ -122,10 +133,12 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     tma_prefetch_desc(&tm_v);
     ring->init(D, 1, 1);
     mbar_init(q_full, 1);
+    mbar_init(q_free, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&p_full[i], 4);
       mbar_init(&o_full[i], 1);
+      mbar_init(&o_free[i], 4);
     }
     fence_barrier_init();
   } else if (warp == 10) {
@@ -142,27 +155,34 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     // ring order = MMA consumption order: K_0, then (K_{j+1}, V_j) for j = 0 .. n1-1
     regs_dec<72>();
     if (lane == 0) {
-      mbar_arrive_expect_tx(q_full, 2 * QTILE);
-#pragma unroll
-      for (int t = 0; t < 2; ++t)
-#pragma unroll
-        for (int h = 0; h < NPANEL; ++h)
-          tma_load_2d(sq + t * QTILE + h * QPANEL, &tm_q, q_full, h * 64, q_row0 + t * A128_BM);
       ArefCursor c;
-      const int kv_row0 = bh * p.S;
-      auto put = [&](const CUtensorMap* m, int blk) {
-        ring->put_acquire(c, 10);
-        ring->put_expect(c, KVTILE);
-        uint8_t* dst = skv + c.slot * KVTILE;
+      for (int it = 0, item = item_of(0); item < num_items; item = item_of(++it)) {
+        int pair, bh;
+        item_coords(item, pair, bh);
+        const int n1 = nblk(pair, 1);
+        const int q_row0 = bh * p.S + pair * 2 * A128_BM;  // row in the [B*H*S, Dh] view
+        const int kv_row0 = bh * p.S;
+        if (it > 0) mbar_wait(q_free, (it - 1) & 1, 9);  // the previous item's QKs have read Q
+        mbar_arrive_expect_tx(q_full, 2 * QTILE);
 #pragma unroll
-        for (int h = 0; h < NPANEL; ++h)
-          tma_load_2d(dst + h * KVPANEL, m, &ring->full[c.slot], h * 64, kv_row0 + blk * A128_BN);
-        c.advance(D);
-      };
-      put(&tm_k, 0);
-      for (int j = 0; j < n1; ++j) {
-        if (j + 1 < n1) put(&tm_k, j + 1);
-        put(&tm_v, j);
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int h = 0; h < NPANEL; ++h)
+            tma_load_2d(sq + t * QTILE + h * QPANEL, &tm_q, q_full, h * 64, q_row0 + t * A128_BM);
+        auto put = [&](const CUtensorMap* m, int blk) {
+          ring->put_acquire(c, 10);
+          ring->put_expect(c, KVTILE);
+          uint8_t* dst = skv + c.slot * KVTILE;
+#pragma unroll
+          for (int h = 0; h < NPANEL; ++h)
+            tma_load_2d(dst + h * KVPANEL, m, &ring->full[c.slot], h * 64, kv_row0 + blk * A128_BN);
+          c.advance(D);
+        };
+        put(&tm_k, 0);
+        for (int j = 0; j < n1; ++j) {
+          if (j + 1 < n1) put(&tm_k, j + 1);
+          put(&tm_v, j);
+        }
       }
     }
   } else if (warp == 9) {
@@ -189,56 +209,68 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
                         (acc || k != 0) ? 1u : 0u);
       }
     };
-    mbar_wait(q_full, 0, 11);
     ArefCursor c;
-    ring->get(c, 12);  // K_0
-    tc_fence_after();
-    issue_qk(0, c.slot);
-    mma_commit_warp(&s_full[0]);
-    issue_qk(1, c.slot);
-    mma_commit_warp(&s_full[1]);
-    mma_commit_warp(&ring->empty[c.slot]);
-    c.advance(D);
-    for (int j = 0; j < n1; ++j) {
-      if (lane == 0) WS_TRACE(0, j, 0);
-      const bool more1 = j + 1 < n1;
-      uint32_t kslot = 0;
-      if (more1) {
-        ring->get(c, 13);  // K_{j+1}
-        kslot = c.slot;
-        c.advance(D);
-      }
-      ring->get(c, 14);  // V_j
-      const uint32_t vslot = c.slot;
+    uint32_t g0 = 0, g1 = 0;  // blocks of tile 0 / tile 1 processed by earlier items
+    for (int it = 0, item = item_of(0); item < num_items; item = item_of(++it)) {
+      int pair, bh;
+      item_coords(item, pair, bh);
+      const int n0 = nblk(pair, 0), n1 = nblk(pair, 1);
+      mbar_wait(q_full, it & 1, 11);
+      ring->get(c, 12);  // K_0
+      tc_fence_after();
+      // S_t is free: the previous item's last PV_t (reading P_t from S_t) was issued before
+      issue_qk(0, c.slot);
+      mma_commit_warp(&s_full[0]);
+      issue_qk(1, c.slot);
+      mma_commit_warp(&s_full[1]);
+      mma_commit_warp(&ring->empty[c.slot]);
       c.advance(D);
-      tc_fence_after();
-      if (lane == 0) WS_TRACE(0, j, 1);
-      if (j < n0) {
-        mbar_wait(&p_full[0], j & 1, 15);  // C_0(j): P_0(j) in TMEM, O_0 rescaled
-        tc_fence_after();
-        if (lane == 0) WS_TRACE(0, j, 2);
-        issue_pv(0, vslot, j > 0);
-        if (j + 1 < n0) {
-          issue_qk(0, kslot);
-          mma_commit_warp(&s_full[0]);
-        } else {
-          mma_commit_warp(&o_full[0]);
+      for (int j = 0; j < n1; ++j) {
+        if (lane == 0) WS_TRACE(0, j, 0);
+        const bool more1 = j + 1 < n1;
+        uint32_t kslot = 0;
+        if (more1) {
+          ring->get(c, 13);  // K_{j+1}
+          kslot = c.slot;
+          c.advance(D);
         }
-        if (lane == 0) WS_TRACE(0, j, 3);
+        ring->get(c, 14);  // V_j
+        const uint32_t vslot = c.slot;
+        c.advance(D);
+        tc_fence_after();
+        if (lane == 0) WS_TRACE(0, j, 1);
+        if (j < n0) {
+          mbar_wait(&p_full[0], (g0 + j) & 1, 15);  // C_0(j): P_0(j) in TMEM, O_0 rescaled
+          if (j == 0 && it > 0) mbar_wait(&o_free[0], (it - 1) & 1, 19);  // previous O_0 copied out
+          tc_fence_after();
+          if (lane == 0) WS_TRACE(0, j, 2);
+          issue_pv(0, vslot, j > 0);
+          if (j + 1 < n0) {
+            issue_qk(0, kslot);
+            mma_commit_warp(&s_full[0]);
+          } else {
+            mma_commit_warp(&o_full[0]);
+          }
+          if (lane == 0) WS_TRACE(0, j, 3);
+        }
+        mbar_wait(&p_full[1], (g1 + j) & 1, 16);
+        if (j == 0 && it > 0) mbar_wait(&o_free[1], (it - 1) & 1, 19);
+        tc_fence_after();
+        if (lane == 0) WS_TRACE(0, j, 4);
+        issue_pv(1, vslot, j > 0);
+        mma_commit_warp(&ring->empty[vslot]);
+        if (more1) {
+          issue_qk(1, kslot);
+          mma_commit_warp(&s_full[1]);
+          mma_commit_warp(&ring->empty[kslot]);
+          if (j + 2 == n1) mma_commit_warp(q_free);  // that was the item's last QK: Q reusable
+        } else {
+          mma_commit_warp(&o_full[1]);
+        }
+        if (lane == 0) WS_TRACE(0, j, 5);
       }
-      mbar_wait(&p_full[1], j & 1, 16);
-      tc_fence_after();
-      if (lane == 0) WS_TRACE(0, j, 4);
-      issue_pv(1, vslot, j > 0);
-      mma_commit_warp(&ring->empty[vslot]);
-      if (more1) {
-        issue_qk(1, kslot);
-        mma_commit_warp(&s_full[1]);
-        mma_commit_warp(&ring->empty[kslot]);
-      } else {
-        mma_commit_warp(&o_full[1]);
-      }
-      if (lane == 0) WS_TRACE(0, j, 5);
+      g0 += n0;
+      g1 += n1;
     }
   } else if (warp >= 8) {
     regs_dec<72>();
@@ -251,15 +283,20 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     const uint32_t t_lane = (q * 32u) << 16;
     const uint32_t t_s = tmem + t_lane + t * A128_BN;
     const uint32_t t_o = tmem + t_lane + COL_O + t * DH;
-    const int n_t = t == 0 ? n0 : n1;
-    const int j_diag = p.causal ? n_t - 1 : -1;
     const float sl2 = p.scale_log2;
+    const bool tr = lane == 0 && q == 0;
+    uint32_t g = 0;  // blocks of this tile processed by earlier items
+    for (int it = 0, item = item_of(0); item < num_items; item = item_of(++it)) {
+    int pair, bh;
+    item_coords(item, pair, bh);
+    const int n_t = nblk(pair, t);
+    const int q_row0 = bh * p.S + pair * 2 * A128_BM;
+    const int j_diag = p.causal ? n_t - 1 : -1;
     float m_used = -INFINITY;  // running max (log2 units) the current P/O are relative to
     float l = 0.f;
-    const bool tr = lane == 0 && q == 0;
     for (int j = 0; j < n_t; ++j) {
       if (tr) WS_TRACE(1 + t, j, 0);
-      mbar_wait(&s_full[t], j & 1, 20 + t);
+      mbar_wait(&s_full[t], (g + j) & 1, 20 + t);
       if (tr) WS_TRACE(1 + t, j, 1);
       tc_fence_after();
       float s[A128_BN];
@@ -357,28 +394,33 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       if (lane == 0) mbar_arrive(&p_full[t]);
       if (tr) WS_TRACE(1 + t, j, 5);
     }
-    // epilogue: O_t / l -> global, lse
-    mbar_wait(&o_full[t], 0, 26 + t);
+    // epilogue: O_t / l -> global, lse. O_t is copied to registers and released (o_free) first, so
+    // the next item's PV_t(0) may overwrite it while this one is converted and stored.
+    g += n_t;
+    mbar_wait(&o_full[t], it & 1, 26 + t);
     tc_fence_after();
+    uint32_t ov[DH];
+#pragma unroll
+    for (int c0 = 0; c0 < DH; c0 += 32) tmem_ld32(t_o + c0, *reinterpret_cast<uint32_t(*)[32]>(ov + c0));
+    tmem_wait_ld();
+    tc_fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&o_free[t]);
     const float inv_l = 1.f / l;
     const size_t grow = static_cast<size_t>(q_row0 + t * A128_BM + row);
     uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) + grow * DH * 2;
-#pragma unroll 1
-    for (int c0 = 0; c0 < DH; c0 += 32) {
-      uint32_t ov[32];
-      tmem_ld32(t_o + c0, ov);
-      tmem_wait_ld();
-      uint32_t w[16];
 #pragma unroll
-      for (int e = 0; e < 16; ++e) {
-        const float a = __uint_as_float(ov[2 * e]) * inv_l, b = __uint_as_float(ov[2 * e + 1]) * inv_l;
+    for (int c0 = 0; c0 < DH; c0 += 8) {
+      uint32_t w[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const float a = __uint_as_float(ov[c0 + 2 * e]) * inv_l, b = __uint_as_float(ov[c0 + 2 * e + 1]) * inv_l;
         w[e] = BF16 ? pack_bf16(a, b) : pack_f16(a, b);
       }
-      uint4* dst = reinterpret_cast<uint4*>(orow + c0 * 2);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) dst[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
+      *reinterpret_cast<uint4*>(orow + c0 * 2) = make_uint4(w[0], w[1], w[2], w[3]);
     }
     if (p.lse) p.lse[grow] = m_used * 0.69314718055994531f + __logf(l);
+    }  // items
   }
 
   tc_fence_before();

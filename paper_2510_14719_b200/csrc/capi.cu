@@ -336,8 +336,8 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
   }
   WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
-  if (PSMEM) {
-    // persistent: one CTA per SM over the (pair, (b,h)) items (attn_psmem_sm100.cuh);
+  {
+    // persistent: one CTA per SM over the (pair, (b,h)) items (both 128-key kernels);
     // WS_ATTN_PERSIST=0 (developer knob) launches one CTA per item instead
     static const int persist_env = [] {
       const char* e = getenv("WS_ATTN_PERSIST");
@@ -345,8 +345,6 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
     }();
     const int items = p.num_pairs * p.num_bh;
     cfg.gridDim = dim3(persist_env == 0 || items < num_sms() ? items : num_sms());
-  } else {
-    cfg.gridDim = p.bh_fast ? dim3(bh1 - bh0, p.num_pairs) : dim3(p.num_pairs, bh1 - bh0);
   }
   cfg.blockDim = dim3(A128_THREADS);
   cfg.dynamicSmemBytes = smem;
