@@ -1,0 +1,22 @@
+"""Small launches of every kernel family for compute-sanitizer (memcheck / racecheck / synccheck).
+  compute-sanitizer --tool racecheck python scripts/sanitize.py"""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch
+import paper_2510_14719_b200 as ws
+
+dev = torch.device("cuda")
+a = torch.randn(512, 1024, device=dev).bfloat16(); b = torch.randn(1024, 1024, device=dev).bfloat16()
+for kw in ({"cta_pair": False}, {"cta_pair": True, "bn": 256}, {"cta_pair": True, "bn": 512}):
+    ws.gemm_tn(a, b, **kw)
+a8, b8 = a.to(torch.float8_e4m3fn), b.to(torch.float8_e4m3fn)
+ws.gemm_tn(a8, b8, cta_pair=True)
+q = torch.randn(1, 2, 512, 128, device=dev).bfloat16(); k = torch.randn_like(q); v = torch.randn_like(q)
+for causal in (False, True):
+    ws.attn_fwd(q, k, v, causal=causal)
+    if not os.environ.get("SKIP_KV64"):
+        ws.attn_fwd(q, k, v, causal=causal, kv_block=64)
+    ws.attn_fwd(q[..., :64].contiguous(), k[..., :64].contiguous(), v[..., :64].contiguous(), causal=causal)
+    ws.attn_fwd(q.to(torch.float8_e4m3fn), k.to(torch.float8_e4m3fn), v.to(torch.float8_e4m3fn), causal=causal)
+torch.cuda.synchronize()
+print("sanitize workload done")
