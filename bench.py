@@ -322,6 +322,30 @@ def run_ours(args):
         roofline["peak_at_sampled_clock"] = round(clk_peak, 1)
         roofline["frac_at_sampled_clock"] = round(achieved / clk_peak, 4)
 
+    # ---- the vendor library on the two dominant GEMM shapes, same box and power state (context
+    # for the headline; not part of `value`) ----
+    lib = {}
+    for K in (8192, 16384):
+        a, b = ops[K]
+        for _ in range(3):
+            torch.matmul(a, b.T, out=c)
+        torch.cuda.synchronize()
+        ms_lib, ms_ours = [], []
+        pair = ((lambda: ws.gemm_tn(a, b, c), ms_ours), (lambda: torch.matmul(a, b.T, out=c), ms_lib))
+        for w in range(6):  # alternating windows (order flipped every window), medians
+            for fn, acc in (pair if w % 2 == 0 else pair[::-1]):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(20):
+                    fn()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                acc.append(e0.elapsed_time(e1) / 20)
+        med = lambda xs: sorted(xs)[len(xs) // 2]
+        lib[f"bf16_8192x8192x{K}"] = {"ours_tflops": round(gemm_flops(K) / (med(ms_ours) * 1e-3) / 1e12, 1),
+                                      "cublas_tflops": round(gemm_flops(K) / (med(ms_lib) * 1e-3) / 1e12, 1),
+                                      "windows": "6 alternating windows of 20 launches each, medians"}
+
     # ---- attention path (C4 / C5), reported beside the headline ----
     attn = bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier)
     other_configs = bench_fp8_and_c1(ws, torch, dev, stream, args, world, max_over_ranks, barrier)
@@ -339,6 +363,7 @@ def run_ours(args):
         "frac_of_peak": round(value / world / peaks["bf16_sustained"], 4),
         "tflops_per_k": per_k,
         "gemm_8192_cubed_tflops": per_k["8192"],
+        "vs_cublas_same_box": lib,
         "attention": attn,
         "other_configs": other_configs,
         "roofline": roofline,
