@@ -183,3 +183,32 @@ def test_fp8_e4m3_rows_sum_to_one(ws, dev):
         o, _ = ws.attn_fwd(q.to(E4M3), k.to(E4M3), v.to(E4M3), causal=causal)
         torch.cuda.synchronize()
         assert (o.float() - 1).abs().max().item() <= 2.0 ** -4
+
+
+@pytest.mark.parametrize("D", [2, 3, 8])
+def test_fp8_e4m3_kv_aref_depths_and_shards(ws, dev, D):
+    """FP8 path: every K/V ring depth gives the same result, and (b,h) shards tile the output."""
+    B, H, S = 2, 3, 768
+    q, k, v = _inputs(B, H, S, 128, torch.float32, dev)
+    q8, k8, v8 = q.to(E4M3), k.to(E4M3), v.to(E4M3)
+    ref_o, ref_l = ws.attn_fwd(q8, k8, v8, causal=True)
+    o, lse = ws.attn_fwd(q8, k8, v8, causal=True, D=D)
+    torch.cuda.synchronize()
+    assert torch.equal(o, ref_o) and torch.equal(lse, ref_l)
+    o2 = torch.full_like(ref_o, float("nan"))
+    l2 = torch.full_like(ref_l, float("nan"))
+    for r in range(4):
+        ws.attn_fwd(q8, k8, v8, causal=True, D=D, out=o2, lse=l2, bh_range=shard.attn_shard(B * H, 4, r))
+    torch.cuda.synchronize()
+    assert torch.equal(o2, ref_o) and torch.equal(l2, ref_l)
+
+
+@pytest.mark.parametrize("kv_block", KV_BLOCKS)
+@pytest.mark.parametrize("Dh", [64, 128])
+def test_single_query_pair(ws, dev, kv_block, Dh):
+    """S = 256: one work item per (b,h) (the causal item has a 1-block tile 0 and a 2-block tile 1)."""
+    q, k, v = _inputs(3, 2, 256, Dh, BF16, dev, qk_div=1.0)
+    for causal in (False, True):
+        o, lse = ws.attn_fwd(q, k, v, causal=causal, kv_block=kv_block)
+        torch.cuda.synchronize()
+        _check(q, k, v, o, lse, causal)

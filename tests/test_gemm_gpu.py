@@ -175,3 +175,12 @@ def test_host_pipeline_matches_device_path_bit_exact(ws, dev):
         ev.synchronize()
         for (_, _, c), w in zip(jobs, want):
             assert np.array_equal(c.numpy().astype(np.float64), w)
+
+
+@pytest.mark.parametrize("D,P", [(2, 2), (3, 3), (4, 4), (3, 1), (4, 2)])
+def test_pair_512_tiles_pipeline_depths(ws, dev, D, P):
+    """256 x 512 pair tiles over several tiles per pair: the half-by-half accumulator hand-over
+    (P = D) and the plain path the literal P window takes (P < D) give the same exact bits."""
+    M, N, K = 2048, 8192, 320  # 128 tiles (~2 per CTA pair), 5 K blocks
+    _, _, c = _run(ws, dev, M, N, K, BF16, F32, cta_pair=True, bn=512, D=D, P=P, persistent=True)
+    assert np.array_equal(as_f64(c), _want(M, N, K))
