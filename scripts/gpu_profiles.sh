@@ -3,8 +3,8 @@
 # (K=16384, 256x512 pair tile) next to cuBLAS, the hdim-128 attention kernel, the FP8 attention kernel
 # and the hdim-64 causal kernel. Reports land in gpurun_out/.
 mkdir -p gpurun_out
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 500 --csv --log-file gpurun_out/launches_final.csv \
-  python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/bench_ncu_final.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 1000 --csv --log-file gpurun_out/launches_final.csv \
+  python bench.py --steps 2 --warmup 3 --no-cpu-baseline --no-vs-cublas > gpurun_out/bench_ncu_final.log 2>&1
 K=16384 EXTRA="--bn 512" bash scripts/prof_gemm_vs_cublas.sh > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:ws_attn -s 1 -c 1 -o gpurun_out/prof_attn_final python scripts/prof_one.py attn > /dev/null 2>&1
 timeout 300 ncu --set full --clock-control none --import-source on -k regex:ws_attn -s 1 -c 1 -o gpurun_out/prof_attn_fp8 python scripts/prof_one.py attn_fp8 > /dev/null 2>&1
