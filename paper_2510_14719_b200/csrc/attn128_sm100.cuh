@@ -72,7 +72,8 @@ __device__ __forceinline__ float fmax3(float a, float b, float c) {
 template <int DH, bool BF16, int POLY = 2, bool TRACE = false>
 __global__ void __launch_bounds__(A128_THREADS, 1)
     ws_attn128_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                      const __grid_constant__ CUtensorMap tm_v, const Attn128Params p) {
+                      const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                      const Attn128Params p) {
   constexpr uint32_t QTILE = A128_BM * DH * 2;   // bytes of a 128 x DH Q tile
   constexpr uint32_t KVTILE = A128_BN * DH * 2;  // bytes of a 128 x DH K or V block
   constexpr uint32_t QPANEL = A128_BM * 128;     // one 64-column (128 B) swizzle panel of Q

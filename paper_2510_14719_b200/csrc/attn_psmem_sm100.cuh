@@ -53,7 +53,8 @@ __host__ __device__ inline uint32_t aps_smem_bytes(int Dh, int kv_stages) {
 template <int DH, bool BF16, int POLY = 2, bool TRACE = false, bool FP8 = false>
 __global__ void __launch_bounds__(A128_THREADS, 1)
     ws_attn_psmem_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
-                         const __grid_constant__ CUtensorMap tm_v, const Attn128Params p) {
+                         const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
+                         const Attn128Params p) {
   constexpr int EB = FP8 ? 1 : 2;                     // operand element bytes
   constexpr uint32_t QTILE = A128_BM * DH * EB;       // bytes of a 128 x DH Q tile
   constexpr uint32_t PTILE = A128_BM * A128_BN * EB;  // bytes of a 128 x 128 P tile
@@ -109,10 +110,10 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
   auto item_of = [&](int r) { return r * G + ((p.causal && (r & 1)) ? G - 1 - b_id : b_id); };
   unsigned long long* const trace =
       (TRACE && p.trace != nullptr && blockIdx.x == 0) ? p.trace : nullptr;
-  // stamps of the first item of CTA 0 only
+  // stamps of CTA 0, indexed by the running block counter across its items
 #define WS_TRACE(role, j, ev)                                                        \
   do {                                                                              \
-    if (TRACE && trace != nullptr && it == 0 && (j) < ATTN_TRACE_STEPS)             \
+    if (TRACE && trace != nullptr && (j) < ATTN_TRACE_STEPS)                        \
       trace[((role) * ATTN_TRACE_STEPS + (j)) * 8 + (ev)] = clk64();                \
   } while (0)
 
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     tma_prefetch_desc(&tm_q);
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
+    tma_prefetch_desc(&tm_o);
     ring->init(D, 1, 1);
     mbar_init(q_full, 1);
     mbar_init(q_free, 1);
@@ -234,7 +236,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       mma_commit_warp(&ring->empty[c.slot]);
       c.advance(D);
       for (int j = 0; j < n1; ++j) {
-        if (lane == 0) WS_TRACE(0, j, 0);
+        if (lane == 0) WS_TRACE(0, g1 + j, 0);
         const bool more = j + 1 < n1;
         uint32_t kslot = 0;
         auto qk1 = [&]() {
@@ -255,10 +257,10 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
             issue_qk(0, kslot);
             mma_commit_warp(&s_full[0]);
           }
-          if (lane == 0) WS_TRACE(0, j, 1);
+          if (lane == 0) WS_TRACE(0, g1 + j, 1);
           if (!p.stagger) qk1();
         }
-        if (lane == 0) WS_TRACE(0, j, 2);
+        if (lane == 0) WS_TRACE(0, g1 + j, 2);
         ring->get(c, 14);  // V_j
         const uint32_t vslot = c.slot;
         c.advance(D);
@@ -266,7 +268,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
           mbar_wait(&p_full[0], (g0 + j) & 1, 15);  // C_0(j): P_0(j) in smem, O_0 rescaled
           if (j == 0 && it > 0) mbar_wait(&o_free[0], (it - 1) & 1, 19);  // previous O_0 copied out
           tc_fence_after();
-          if (lane == 0) WS_TRACE(0, j, 3);
+          if (lane == 0) WS_TRACE(0, g1 + j, 3);
           issue_pv(0, vslot, j > 0);
           mma_commit_warp(&pv_done[0]);
         }
@@ -277,11 +279,11 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         mbar_wait(&p_full[1], (g1 + j) & 1, 16);
         if (j == 0 && it > 0) mbar_wait(&o_free[1], (it - 1) & 1, 19);
         tc_fence_after();
-        if (lane == 0) WS_TRACE(0, j, 4);
+        if (lane == 0) WS_TRACE(0, g1 + j, 4);
         issue_pv(1, vslot, j > 0);
         mma_commit_warp(&pv_done[1]);
         mma_commit_warp(&ring->empty[vslot]);
-        if (lane == 0) WS_TRACE(0, j, 5);
+        if (lane == 0) WS_TRACE(0, g1 + j, 5);
       }
       g0 += n0;
       g1 += n1;
@@ -312,9 +314,9 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     float m_used = -INFINITY;  // running max (log2 units) the current P/O are relative to
     float l = 0.f;
     for (int j = 0; j < n_t; ++j) {
-      if (tr) WS_TRACE(1 + t, j, 0);
+      if (tr) WS_TRACE(1 + t, g + j, 0);
       mbar_wait(&s_full[t], (g + j) & 1, 20 + t);
-      if (tr) WS_TRACE(1 + t, j, 1);
+      if (tr) WS_TRACE(1 + t, g + j, 1);
       tc_fence_after();
       float s[A128_BN];
       {
@@ -327,7 +329,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_free[t]);
-      if (tr) WS_TRACE(1 + t, j, 2);
+      if (tr) WS_TRACE(1 + t, g + j, 2);
       if (j == j_diag) {
 #pragma unroll
         for (int c = 0; c < A128_BN; ++c) s[c] = c > row ? -INFINITY : s[c];
@@ -377,10 +379,15 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         tmem_wait_st();
       }
       l *= alpha;
-      if (tr) WS_TRACE(1 + t, j, 3);
+      if (tr) WS_TRACE(1 + t, g + j, 3);
       // P_t's shared-memory tile is free once PV_t(j-1) has read it (long done by now: PV_t(j-1) was
       // issued when this warp finished block j-1)
       if (g + j > 0) mbar_wait(&pv_done[t], (g + j - 1) & 1, 24 + t);
+      if (j == 0 && it > 0) {
+        // the previous item's O_t was staged through this P tile: its TMA store must have read it
+        if (warp == 4u * t && lane == 0) tma_store_wait_read<0>();
+        named_bar_sync(1 + t, 128);
+      }
       // P = 2^(s*sl2 - m), packed to 16-bit pairs and stored 8 keys (16 bytes) at a time into the
       // 128B-swizzled K-major P tile as it is produced, so the shared-memory writes overlap the math
       const uint64_t sl2x2 = f2_pack(sl2, sl2), negm2 = f2_pack(-m_used, -m_used);
@@ -422,12 +429,12 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         f2_unpack(f2_add(sum4[2], sum4[3]), c2, d2);
         l += (a + b) + (c2 + d2);
       }
-      if (tr) WS_TRACE(1 + t, j, 4);
+      if (tr) WS_TRACE(1 + t, g + j, 4);
       fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core's reads
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&p_full[t]);
-      if (tr) WS_TRACE(1 + t, j, 5);
+      if (tr) WS_TRACE(1 + t, g + j, 5);
     }
     // epilogue: O_t / l -> global, lse once the last PV_t has completed. O_t is copied to registers
     // first and released (o_free) so the next item's PV_t(0) can overwrite it while this finishes.
@@ -443,19 +450,43 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     if (lane == 0) mbar_arrive(&o_free[t]);
     const float inv_l = p.o_scale / l;  // V's per-tensor descale (FP8) folded into 1 / l
     const size_t grow = static_cast<size_t>(q_row0 + t * A128_BM + row);
-    uint8_t* orow = reinterpret_cast<uint8_t*>(p.o) + grow * DH * 2;
+    // O_t leaves through TMA: each thread writes its row (16-bit, 128B-swizzled, 64 columns per
+    // 16 KB panel) into this tile's P buffer — free, since its last PV has completed — and one
+    // thread stores the 128 x 64 boxes. A thread writing its own 256-byte row straight to global
+    // memory would issue 32 scattered 16-byte writes per warp instruction; that epilogue cost
+    // ~7000 cycles per work item (scripts/attn_trace_items.py).
+    constexpr int OPANELS = DH / 64;                          // 64 output columns per panel
+    constexpr int PPANELS = static_cast<int>(PTILE / PANEL);  // staging panels in the P tile
+    const uint32_t ptile = smem_u32(sp + t * PTILE);
 #pragma unroll
-    for (int c0 = 0; c0 < DH; c0 += 8) {
-      uint32_t w[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float a = __uint_as_float(ov[c0 + 2 * e]) * inv_l, b = __uint_as_float(ov[c0 + 2 * e + 1]) * inv_l;
-        w[e] = (BF16 || FP8) ? pack_bf16(a, b) : pack_f16(a, b);
+    for (int c = 0; c < OPANELS; ++c) {
+      const uint32_t buf = ptile + (c % PPANELS) * PANEL;
+      if (c >= PPANELS) {  // reuse of a staging panel: its previous store must have read it
+        if (warp == 4u * t && lane == 0) tma_store_wait_read<0>();
+        named_bar_sync(1 + t, 128);
       }
-      *reinterpret_cast<uint4*>(orow + c0 * 2) = make_uint4(w[0], w[1], w[2], w[3]);
+#pragma unroll
+      for (int k8 = 0; k8 < 8; ++k8) {
+        uint32_t w[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int col = c * 64 + k8 * 8 + 2 * e;
+          const float a = __uint_as_float(ov[col]) * inv_l, b = __uint_as_float(ov[col + 1]) * inv_l;
+          w[e] = (BF16 || FP8) ? pack_bf16(a, b) : pack_f16(a, b);
+        }
+        st_shared_v4(buf + row * 128u + ((static_cast<uint32_t>(k8) ^ swz) << 4), w[0], w[1], w[2], w[3]);
+      }
+      fence_proxy_async_smem();
+      named_bar_sync(1 + t, 128);
+      if (warp == 4u * t && lane == 0) {
+        tma_store_2d(&tm_o, reinterpret_cast<const void*>(sp + t * PTILE + (c % PPANELS) * PANEL), c * 64,
+                     q_row0 + t * A128_BM);
+        tma_store_commit();
+      }
     }
     if (p.lse) p.lse[grow] = m_used * 0.69314718055994531f + __logf(l);
     }  // items
+    if (warp == 4u * t && lane == 0) tma_store_wait<0>();  // O stores complete before the CTA retires
   }
 
   tc_fence_before();

@@ -323,6 +323,9 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
     const char* e = getenv("WS_ATTN_POLY");
     return e ? atoi(e) : -1;
   }();
+  // O [B*H*S, DH] in the input's 16-bit type, stored through TMA in 128 x 64 boxes
+  CUtensorMap to;
+  if ((s = make_tmap(&to, d.O, dt, rows, DH, DH, A128_BM, 64, CU_TENSOR_MAP_L2_PROMOTION_NONE)) != WS_OK) return s;
   auto kern = trace ? ws_attn128_kernel<DH, BF16, A128_POLY, true> : ws_attn128_kernel<DH, BF16, A128_POLY>;
   if (PSMEM)
     kern = trace ? ws_attn_psmem_kernel<DH, BF16, APS_POLY, true> : ws_attn_psmem_kernel<DH, BF16, APS_POLY>;
@@ -350,7 +353,7 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   apply_wait_hint();
-  WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, p));
+  WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, to, p));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return WS_OK;
 }
@@ -396,6 +399,9 @@ ws_status launch_attn_fp8(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t 
     return s;
   if ((s = make_tmap(&tv, d.V, WS_E4M3, rows, DH, DH, A128_BN, 128, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
     return s;
+  CUtensorMap to;  // O in bf16
+  if ((s = make_tmap(&to, d.O, WS_BF16, rows, DH, DH, A128_BM, 64, CU_TENSOR_MAP_L2_PROMOTION_NONE)) != WS_OK)
+    return s;
   auto kern = trace ? ws_attn_psmem_kernel<DH, true, APS_POLY, true, true> : ws_attn_psmem_kernel<DH, true, APS_POLY, false, true>;
   WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
@@ -405,7 +411,7 @@ ws_status launch_attn_fp8(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t 
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   apply_wait_hint();
-  WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, p));
+  WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, to, p));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return WS_OK;
 }
