@@ -214,27 +214,40 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     };
     ArefCursor c;
     uint32_t g0 = 0, g1 = 0;  // blocks of tile 0 / tile 1 processed by earlier items
+    // First QK of tile 0 of item `it` (K_0 taken from the ring, its slot kept for tile 1's QK). It
+    // is issued inside the previous item's last step, right after that item's last PV_0, so the
+    // next item's first S_0 is computed while tile 1 finishes the current item (cross-item
+    // software pipelining of the T stage; Q of item it was loaded after the previous item's last
+    // QK released it).
+    uint32_t k0slot = 0;
+    auto first_qk0 = [&](int it_, uint32_t g0_) {
+      mbar_wait(q_full, it_ & 1, 11);
+      ring->get(c, 12);  // K_0
+      k0slot = c.slot;
+      c.advance(D);
+      tc_fence_after();
+      if (g0_ > 0) {
+        mbar_wait(&s_free[0], (g0_ - 1) & 1, 17);  // the previous item's last S_0 copied out
+        tc_fence_after();
+      }
+      issue_qk(0, k0slot);
+      mma_commit_warp(&s_full[0]);
+    };
+    bool qk0_issued = false;
     for (int it = 0, item = item_of(0); item < num_items; item = item_of(++it)) {
       int pair, bh;
       item_coords(item, pair, bh);
       const int n0 = nblk(pair, 0), n1 = nblk(pair, 1);
-      mbar_wait(q_full, it & 1, 11);
-      ring->get(c, 12);  // K_0
-      tc_fence_after();
-      if (g0 > 0) {
-        mbar_wait(&s_free[0], (g0 - 1) & 1, 17);  // the previous item's last S_0 copied out
-        tc_fence_after();
-      }
-      issue_qk(0, c.slot);
-      mma_commit_warp(&s_full[0]);
+      if (!qk0_issued) first_qk0(it, g0);
+      qk0_issued = false;
       if (g1 > 0) {
         mbar_wait(&s_free[1], (g1 - 1) & 1, 18);
         tc_fence_after();
       }
-      issue_qk(1, c.slot);
+      issue_qk(1, k0slot);
       mma_commit_warp(&s_full[1]);
-      mma_commit_warp(&ring->empty[c.slot]);
-      c.advance(D);
+      mma_commit_warp(&ring->empty[k0slot]);
+      const int next_item = item_of(it + 1);
       for (int j = 0; j < n1; ++j) {
         if (lane == 0) WS_TRACE(0, g1 + j, 0);
         const bool more = j + 1 < n1;
@@ -276,6 +289,10 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         // two softmax warpgroups' latency-bound phases (row max) interleave with the other's
         // exponentials instead of coinciding
         if (more && p.stagger) qk1();
+        if (!more && next_item < num_items) {
+          first_qk0(it + 1, g0 + n0);  // the next item's T_0(0), ahead of this item's last PV_1
+          qk0_issued = true;
+        }
         mbar_wait(&p_full[1], (g1 + j) & 1, 16);
         if (j == 0 && it > 0) mbar_wait(&o_free[1], (it - 1) & 1, 19);
         tc_fence_after();
@@ -448,6 +465,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     tc_fence_before();
     __syncwarp();
     if (lane == 0) mbar_arrive(&o_free[t]);
+    if (tr) WS_TRACE(1 + t, g - 1, 6);
     const float inv_l = p.o_scale / l;  // V's per-tensor descale (FP8) folded into 1 / l
     const size_t grow = static_cast<size_t>(q_row0 + t * A128_BM + row);
     // O_t leaves through TMA: each thread writes its row (16-bit, 128B-swizzled, 64 columns per
@@ -485,6 +503,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       }
     }
     if (p.lse) p.lse[grow] = m_used * 0.69314718055994531f + __logf(l);
+    if (tr) WS_TRACE(1 + t, g - 1, 7);
     }  // items
     if (warp == 4u * t && lane == 0) tma_store_wait<0>();  // O stores complete before the CTA retires
   }

@@ -20,6 +20,10 @@ for (B, S) in ((16, 1024), (4, 4096), (1, 16384)):
     dur = lambda g: int(t[1, g + 1, 1] - t[1, g, 1])     # softmax-0 S-arrival to next S-arrival
     wait = lambda g: int(t[1, g, 1] - t[1, g, 0])        # softmax-0 waiting for S
     epi = lambda g: int(t[1, g, 0] - t[1, g - 1, 5])     # gap before the wait (the epilogue when g % nb == 0)
+    last = [g - 1 for g in first]
+    ep_ld = statistics.median(int(t[1, g, 6] - t[1, g, 5]) for g in last) if last else "-"
+    ep_st = statistics.median(int(t[1, g, 7] - t[1, g, 6]) for g in last) if last else "-"
+    print(f"  epilogue: last p_full -> O in registers {ep_ld}, -> staged + TMA issued {ep_st}")
     print(f"S={S} B={B}: steps/item {nb}; first-step of item: period {statistics.median(dur(g - 1) for g in first) if first else '-'} "
           f"wait {statistics.median(wait(g) for g in first) if first else '-'} gap {statistics.median(epi(g) for g in first) if first else '-'}; "
           f"other steps: period {statistics.median(dur(g) for g in rest)} wait {statistics.median(wait(g) for g in rest)} "
