@@ -9,7 +9,8 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libws.so")
+# WS_LIB overrides the library path (developer A/B of two builds, scripts/attn_ab.py)
+LIB_PATH = os.environ.get("WS_LIB") or os.path.join(_HERE, "libws.so")
 
 # ws_status values; 1..12 follow warpspec::ErrorCode (ref proj/include/warpspec/errors.hpp:10-23)
 STATUS_NAMES = {

@@ -335,35 +335,50 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       mbar_wait(&s_full[t], (g + j) & 1, 20 + t);
       if (tr) WS_TRACE(1 + t, g + j, 1);
       tc_fence_after();
+      // S in two halves: the row max of the first 64 columns runs while the second half is loading
+      // (a tcgen05.wait::ld covers every outstanding load, so the halves are waited separately)
       float s[A128_BN];
-      {
-        uint32_t* su = reinterpret_cast<uint32_t*>(s);
+      uint32_t* su = reinterpret_cast<uint32_t*>(s);
+      tmem_ld32(t_s + 0, *reinterpret_cast<uint32_t(*)[32]>(su + 0));
+      tmem_ld32(t_s + 32, *reinterpret_cast<uint32_t(*)[32]>(su + 32));
+      tmem_wait_ld();
+      tmem_ld32(t_s + 64, *reinterpret_cast<uint32_t(*)[32]>(su + 64));
+      tmem_ld32(t_s + 96, *reinterpret_cast<uint32_t(*)[32]>(su + 96));
+      const bool diag = j == j_diag;
+      if (diag) {
 #pragma unroll
-        for (int c0 = 0; c0 < A128_BN; c0 += 32) tmem_ld32(t_s + c0, *reinterpret_cast<uint32_t(*)[32]>(su + c0));
-        tmem_wait_ld();
+        for (int c = 0; c < A128_BN / 2; ++c) s[c] = c > row ? -INFINITY : s[c];
       }
+      float m4[4] = {fmax3(s[0], s[1], s[2]), fmax3(s[3], s[4], s[5]), fmax3(s[6], s[7], s[8]),
+                     fmax3(s[9], s[10], s[11])};
+#pragma unroll
+      for (int c = 12; c + 8 <= A128_BN / 2; c += 8) {
+        m4[0] = fmax3(m4[0], s[c], s[c + 1]);
+        m4[1] = fmax3(m4[1], s[c + 2], s[c + 3]);
+        m4[2] = fmax3(m4[2], s[c + 4], s[c + 5]);
+        m4[3] = fmax3(m4[3], s[c + 6], s[c + 7]);
+      }
+      m4[0] = fmax3(m4[0], s[60], s[61]);
+      m4[1] = fmax3(m4[1], s[62], s[63]);
+      tmem_wait_ld();
       // S_t(j) is in registers: release the TMEM columns so QK_t(j+1) can run during this softmax
       tc_fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&s_free[t]);
       if (tr) WS_TRACE(1 + t, g + j, 2);
-      if (j == j_diag) {
+      if (diag) {
 #pragma unroll
-        for (int c = 0; c < A128_BN; ++c) s[c] = c > row ? -INFINITY : s[c];
+        for (int c = A128_BN / 2; c < A128_BN; ++c) s[c] = c > row ? -INFINITY : s[c];
       }
       float mx;
       {
-        float m4[4] = {fmax3(s[0], s[1], s[2]), fmax3(s[3], s[4], s[5]), fmax3(s[6], s[7], s[8]),
-                       fmax3(s[9], s[10], s[11])};
 #pragma unroll
-        for (int c = 12; c + 8 <= A128_BN; c += 8) {
+        for (int c = A128_BN / 2; c + 8 <= A128_BN; c += 8) {
           m4[0] = fmax3(m4[0], s[c], s[c + 1]);
           m4[1] = fmax3(m4[1], s[c + 2], s[c + 3]);
           m4[2] = fmax3(m4[2], s[c + 4], s[c + 5]);
           m4[3] = fmax3(m4[3], s[c + 6], s[c + 7]);
         }
-        m4[0] = fmax3(m4[0], s[A128_BN - 4], s[A128_BN - 3]);
-        m4[1] = fmax3(m4[1], s[A128_BN - 2], s[A128_BN - 1]);
         mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
       }
       const float m_blk = mx * sl2;
