@@ -327,8 +327,11 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
   CUtensorMap to;
   if ((s = make_tmap(&to, d.O, dt, rows, DH, DH, A128_BM, 64, CU_TENSOR_MAP_L2_PROMOTION_NONE)) != WS_OK) return s;
   auto kern = trace ? ws_attn128_kernel<DH, BF16, A128_POLY, true> : ws_attn128_kernel<DH, BF16, A128_POLY>;
+  // exp mix of the P-in-smem kernel: 1/8 of the pairs on the FMA pipe at hdim 128, 2/8 at hdim 64
+  // (where the softmax alone bounds the kernel; scripts/attn_ab.py)
+  constexpr int PS_POLY = DH == 64 ? 2 : APS_POLY;
   if (PSMEM)
-    kern = trace ? ws_attn_psmem_kernel<DH, BF16, APS_POLY, true> : ws_attn_psmem_kernel<DH, BF16, APS_POLY>;
+    kern = trace ? ws_attn_psmem_kernel<DH, BF16, PS_POLY, true> : ws_attn_psmem_kernel<DH, BF16, PS_POLY>;
   if (BF16 && !trace) {
     switch (poly_env) {
       case 1: kern = PSMEM ? ws_attn_psmem_kernel<DH, BF16, 1> : ws_attn128_kernel<DH, BF16, 1>; break;
@@ -437,14 +440,15 @@ ws_status attn_entry(const ws_attn_desc& d, cudaStream_t st, unsigned long long*
     return launch_attn_fp8(d, bh0, bh1, st, trace);
   }
   if (d.kv_block != 64) {
-    // P staging: hdim 128 stages P in shared memory (S released early, QK_{j+1} overlaps the
-    // softmax); hdim 64 keeps P in TMEM (its shared-memory P tiles would leave less room for the
-    // K/V ring and its PV is operand-bound in SS form). WS_ATTN_PTMEM=0/1 overrides (developer knob).
+    // P staging: P in shared memory (S released right after the softmax copies it, QK_{j+1}
+    // overlaps the softmax, persistent with TMA epilogue) for both head dims; P in TMEM
+    // (attn128_sm100.cuh) measured 3-7% slower at hdim 64 and 2-5% at hdim 128 once the former
+    // had its item-boundary fixes. WS_ATTN_PTMEM=1 selects it (developer knob).
     static const int ptmem_env = [] {
       const char* e = getenv("WS_ATTN_PTMEM");
       return e ? atoi(e) : -1;
     }();
-    const bool ptmem = ptmem_env >= 0 ? ptmem_env == 1 : d.Dh == 64;
+    const bool ptmem = ptmem_env == 1;
     if (ptmem) {
       if (d.Dh == 128)
         return d.dtype == WS_BF16 ? launch_attn128<128, true, false>(d, bh0, bh1, st, trace)

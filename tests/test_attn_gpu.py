@@ -38,7 +38,7 @@ def _check(q, k, v, o, lse, causal, pid_range=None, block=128, tol_o=1e-2, tol_l
     return err_o, err_l
 
 
-KV_BLOCKS = [128, 64]  # 128: attn_psmem (hdim 128) / attn128 (hdim 64) kernels; 64: attn_sm100.cuh
+KV_BLOCKS = [128, 64]  # 128: attn_psmem_sm100.cuh (P-in-TMEM variant: test_p_in_tmem_kernel_via_knob); 64: attn_sm100.cuh
 
 
 @pytest.mark.parametrize("kv_block", KV_BLOCKS)
@@ -212,3 +212,30 @@ def test_single_query_pair(ws, dev, kv_block, Dh):
         o, lse = ws.attn_fwd(q, k, v, causal=causal, kv_block=kv_block)
         torch.cuda.synchronize()
         _check(q, k, v, o, lse, causal)
+
+
+def test_p_in_tmem_kernel_via_knob(ws, dev):
+    """The P-in-TMEM kernel (attn128_sm100.cuh) is selected only by the WS_ATTN_PTMEM=1 developer
+    knob (read once per process), so its parity runs in a child process: hdim 64/128, causal or
+    not, bf16/f16, several work items per CTA."""
+    import os
+    import subprocess
+    import sys
+
+    code = r"""
+import numpy as np, torch, oracle, paper_2510_14719_b200 as ws
+from tests.gpu_helpers import as_f64, ref_tensor, rel_err
+for Dh in (64, 128):
+    for causal in (False, True):
+        for dt in (torch.bfloat16, torch.float16):
+            q, k, v = (ref_tensor(n, (2, 16, 512, Dh), dt, 'cuda', div=d) for n, d in (('q', 1.0), ('k', 1.0), ('v', 4.0)))
+            o, lse = ws.attn_fwd(q, k, v, causal=causal)
+            torch.cuda.synchronize()
+            ro, rl = oracle.flash(as_f64(q), as_f64(k), as_f64(v), causal)
+            assert rel_err(as_f64(o), ro) <= 1e-2 and np.abs(as_f64(lse) - rl).max() <= 1e-3, (Dh, causal, dt)
+print('ok')
+"""
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, WS_ATTN_PTMEM="1", PYTHONPATH=root)
+    out = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0 and out.stdout.strip().endswith("ok"), out.stderr[-2000:]
