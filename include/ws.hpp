@@ -1,0 +1,78 @@
+/*
+ * ws.hpp — reference-side C++ binding of the B200 path: the reference's own types in and out.
+ *
+ * Header-only; include it next to the reference's headers (it uses warpspec::Buffers / Tile /
+ * KernelGraph / CompileError from proj/include/warpspec). It is the `ws::run` shim of SURVEY.md §7
+ * step 2: a `.k` kernel text plus the reference's by-value Buffers (ref
+ * proj/include/warpspec/interp.hpp:31) go to the GPU through the C-ABI in ws.h and come back as
+ * Buffers, so the reference's check pattern applies unchanged — run_compiled compares the
+ * simulator's buffers with interpret_sequential's (ref proj/include/warpspec/driver.hpp:242-266);
+ * here `ws::run(text, inputs, launch) == interpret_tiles(...)`.
+ *
+ * Errors: a non-OK ws_status is rethrown as warpspec::CompileError with the mirrored ErrorCode
+ * (ws_status 1..12 = ErrorCode order + 1, ref proj/include/warpspec/errors.hpp:10-23); CUDA
+ * failures as std::runtime_error — the reference CLI's exit-code split (tools/warpspec.cpp:95-101).
+ */
+#ifndef WS_HPP_
+#define WS_HPP_
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "warpspec/errors.hpp"
+#include "warpspec/interp.hpp"
+#include "warpspec/validate.hpp"
+#include "ws.h"
+
+namespace ws {
+
+struct Launch {
+  int64_t pid_lo = 0;      // the .k pid range to run, like interpret_tiles' tile loop
+  int64_t pid_hi = 1;
+  int32_t dtype = WS_BF16; // device storage type of the real payloads (exact for the reference's)
+  void* stream = nullptr;  // cudaStream_t; the call is synchronous w.r.t. the host buffers
+};
+
+inline void check(ws_status s) {
+  if (s == WS_OK) return;
+  const std::string msg = ws_last_error();
+  if (s >= WS_PARSE && s <= WS_EVAL)
+    throw warpspec::CompileError(static_cast<warpspec::ErrorCode>(static_cast<int>(s) - 1), msg);
+  throw std::runtime_error("ws: " + msg);
+}
+
+// Run pids [launch.pid_lo, launch.pid_hi) of `ktext` on the GPU. Parameters missing from `inputs`
+// start zeroed (ref interp.hpp:140-154 prepare_buffers); every parameter is returned.
+inline warpspec::Buffers run(const std::string& ktext, const warpspec::Buffers& inputs, const Launch& launch = {}) {
+  const warpspec::KernelGraph g = warpspec::parse_kernel(ktext);  // the reference's own front end
+  warpspec::Buffers out;
+  std::vector<ws_kbuffer> bufs;
+  bufs.reserve(g.params.size());
+  for (const auto& p : g.params) {
+    auto it = inputs.find(p.name);
+    warpspec::Tile t = it != inputs.end() ? it->second : warpspec::Tile(p.type);
+    if (t.type != p.type)
+      throw warpspec::CompileError(warpspec::ErrorCode::Type, "buffer " + p.name + " is " + t.type.str() +
+                                                                  ", the kernel declares " + p.type.str());
+    out[p.name] = std::move(t);
+  }
+  for (const auto& p : g.params) {
+    warpspec::Tile& t = out[p.name];
+    ws_kbuffer b{};
+    b.name = p.name.c_str();
+    b.rows = t.type.rows;
+    b.cols = t.type.cols;
+    b.is_real = t.type.elem == warpspec::Elem::Real;
+    b.data = b.is_real ? static_cast<void*>(t.rv.data()) : static_cast<void*>(t.iv.data());
+    bufs.push_back(b);
+  }
+  check(ws_run_kernel(ktext.c_str(), bufs.data(), static_cast<int32_t>(bufs.size()), launch.pid_lo, launch.pid_hi,
+                      launch.dtype, launch.stream));
+  return out;
+}
+
+}  // namespace ws
+
+#endif  // WS_HPP_
