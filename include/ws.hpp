@@ -7,7 +7,7 @@
  * proj/include/warpspec/interp.hpp:31) go to the GPU through the C-ABI in ws.h and come back as
  * Buffers, so the reference's check pattern applies unchanged — run_compiled compares the
  * simulator's buffers with interpret_sequential's (ref proj/include/warpspec/driver.hpp:242-266);
- * here `ws::run(text, inputs, launch) == interpret_tiles(...)`.
+ * here `ws::run(text, inputs, launch) == interpret_tiles(...)`, or `ws::run(graph, inputs, launch)`.
  *
  * Errors: a non-OK ws_status is rethrown as warpspec::CompileError with the mirrored ErrorCode
  * (ws_status 1..12 = ErrorCode order + 1, ref proj/include/warpspec/errors.hpp:10-23); CUDA
@@ -23,6 +23,7 @@
 
 #include "warpspec/errors.hpp"
 #include "warpspec/interp.hpp"
+#include "warpspec/print.hpp"
 #include "warpspec/validate.hpp"
 #include "ws.h"
 
@@ -43,10 +44,10 @@ inline void check(ws_status s) {
   throw std::runtime_error("ws: " + msg);
 }
 
-// Run pids [launch.pid_lo, launch.pid_hi) of `ktext` on the GPU. Parameters missing from `inputs`
-// start zeroed (ref interp.hpp:140-154 prepare_buffers); every parameter is returned.
-inline warpspec::Buffers run(const std::string& ktext, const warpspec::Buffers& inputs, const Launch& launch = {}) {
-  const warpspec::KernelGraph g = warpspec::parse_kernel(ktext);  // the reference's own front end
+namespace detail {
+// Marshal `inputs` against the graph's declared parameters and run `ktext` (the graph's text).
+inline warpspec::Buffers run_graph(const warpspec::KernelGraph& g, const std::string& ktext,
+                                   const warpspec::Buffers& inputs, const Launch& launch) {
   warpspec::Buffers out;
   std::vector<ws_kbuffer> bufs;
   bufs.reserve(g.params.size());
@@ -71,6 +72,22 @@ inline warpspec::Buffers run(const std::string& ktext, const warpspec::Buffers& 
   check(ws_run_kernel(ktext.c_str(), bufs.data(), static_cast<int32_t>(bufs.size()), launch.pid_lo, launch.pid_hi,
                       launch.dtype, launch.stream));
   return out;
+}
+}  // namespace detail
+
+// Run pids [launch.pid_lo, launch.pid_hi) of `ktext` on the GPU. Parameters missing from `inputs`
+// start zeroed (ref interp.hpp:140-154 prepare_buffers); every parameter is returned.
+inline warpspec::Buffers run(const std::string& ktext, const warpspec::Buffers& inputs, const Launch& launch = {}) {
+  return detail::run_graph(warpspec::parse_kernel(ktext), ktext, inputs, launch);  // the reference's front end
+}
+
+// SURVEY.md §8b's shim signature: a parsed KernelGraph in, Buffers out. The graph is printed back
+// to `.k` text by the reference's own printer (ref proj/include/warpspec/print.hpp:160), the form
+// the C-ABI takes. Not re-parsed by parse_kernel: the reference's parser rejects its printer's
+// exponent form for constants such as -1e6 ("[[-1e+06]]"); the C-ABI's front end accepts it.
+inline warpspec::Buffers run(const warpspec::KernelGraph& g, const warpspec::Buffers& inputs,
+                             const Launch& launch = {}) {
+  return detail::run_graph(g, warpspec::print_kernel(g), inputs, launch);
 }
 
 }  // namespace ws

@@ -88,8 +88,16 @@ int main(int argc, char** argv) {
       l.pid_lo = 0;
       l.pid_hi = n;
       const warpspec::Buffers got = ws::run(text, inputs, l);
+      // the KernelGraph overload (printed back to text by the reference's printer) must give the
+      // same buffers bit for bit
+      const warpspec::Buffers got_g = ws::run(g, inputs, l);
       std::string why;
       bool ok;
+      if (!exact(got, got_g, why)) {
+        std::printf("FAIL %s: ws::run(KernelGraph) differs from ws::run(text): %s\n", f.c_str(), why.c_str());
+        ++failures;
+        continue;
+      }
       if (!flash) {
         ok = exact(want, got, why);
       } else {

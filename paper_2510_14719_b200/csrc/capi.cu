@@ -405,7 +405,23 @@ ws_status launch_attn_fp8(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t 
   CUtensorMap to;  // O in bf16
   if ((s = make_tmap(&to, d.O, WS_BF16, rows, DH, DH, A128_BM, 64, CU_TENSOR_MAP_L2_PROMOTION_NONE)) != WS_OK)
     return s;
-  auto kern = trace ? ws_attn_psmem_kernel<DH, true, APS_POLY, true, true> : ws_attn_psmem_kernel<DH, true, APS_POLY, false, true>;
+  // exp mix 2 of every 8 pairs on the FMA pipe: with the tensor work halved the softmax alone bounds
+  // FP8 (POLY 0/1/2/3/4 = 1586/1614/1645/1539/1483 TFLOP/s at S=16K, scripts/attn_ab.py AB_FP8=1)
+  constexpr int F8_POLY = 2;
+  auto kern = trace ? ws_attn_psmem_kernel<DH, true, F8_POLY, true, true> : ws_attn_psmem_kernel<DH, true, F8_POLY, false, true>;
+  static const int poly_env = [] {
+    const char* e = getenv("WS_ATTN_POLY");
+    return e ? atoi(e) : -1;
+  }();
+  if (!trace) {
+    switch (poly_env) {
+      case 0: kern = ws_attn_psmem_kernel<DH, true, 0, false, true>; break;
+      case 1: kern = ws_attn_psmem_kernel<DH, true, 1, false, true>; break;
+      case 3: kern = ws_attn_psmem_kernel<DH, true, 3, false, true>; break;
+      case 4: kern = ws_attn_psmem_kernel<DH, true, 4, false, true>; break;
+      default: break;
+    }
+  }
   WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   cudaLaunchConfig_t cfg = {};
   const int items = p.num_pairs * p.num_bh;

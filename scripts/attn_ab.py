@@ -2,7 +2,8 @@
 
 Each variant runs in a subprocess (the knobs are read once per process); rounds alternate so
 clock/power drift hits every variant alike.
-  python scripts/attn_ab.py 'WS_ATTN_PTMEM=1' 'WS_ATTN_PTMEM=0' ..."""
+  python scripts/attn_ab.py 'WS_ATTN_PTMEM=1' 'WS_ATTN_PTMEM=0' ...
+AB_FP8=1 runs the hdim-128 cases with e4m3 inputs."""
 import json, os, subprocess, sys
 
 CODE = r'''
@@ -10,9 +11,13 @@ import sys, os, json, torch
 sys.path.insert(0, os.getcwd())
 import paper_2510_14719_b200 as ws
 res = {}
-for (B, S, Dh, causal) in [(1, 16384, 128, False), (1, 16384, 128, True), (16, 1024, 128, False), (1, 16384, 64, True), (1, 16384, 64, False)]:
+fp8 = os.environ.get("AB_FP8") == "1"
+cases = [(1, 16384, 128, False), (1, 16384, 128, True), (16, 1024, 128, False), (1, 16384, 64, True), (1, 16384, 64, False)]
+for (B, S, Dh, causal) in (cases[:3] if fp8 else cases):
     q = torch.randn(B, 16, S, Dh, device="cuda", dtype=torch.bfloat16); k = torch.randn_like(q); v = torch.randn_like(q)
     o = torch.empty_like(q); lse = torch.empty(B, 16, S, device="cuda")
+    if fp8:
+        q, k, v = (t.to(torch.float8_e4m3fn) for t in (q, k, v))
     for _ in range(3): ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse)
     torch.cuda.synchronize()
     e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
