@@ -35,9 +35,10 @@ K_SWEEP = [256, 512, 1024, 2048, 4096, 8192, 16384]
 METRIC = "GEMM & attention-fwd TFLOPS at 1/2/4/8 B200, % of tensor-core peak"
 WORKLOAD = ("C2: bf16 GEMM c = a.b^T, M=N=8192 (per GPU; global N = 8192*n_gpus), "
             "K sweep 256..16384, one pass = 7 launches")
-TILE_POLICY = ("library auto policy: K<512: 128x256x64 single-CTA tiles (D=4, raster group 4); 512<=K<4096: "
-               "256x256x64 cta_group::2 pairs (D=6, group 2, TMEM double-buffered); K>=4096: 256x512x64 pairs "
-               "(D=4, group 16, one TMEM accumulator)")
+TILE_POLICY = ("library auto policy: cta_group::2 CTA pairs (M % 256 == 0, K >= 256); < 16 K blocks (K < 1024): "
+               "256x256x64 pair tiles (D=6, raster group 2, TMEM double-buffered); >= 16 K blocks: 256x512x64 "
+               "pair tiles (D=4, group 16, one TMEM accumulator handed over N half by N half, early-release "
+               "epilogue)")
 
 
 def gemm_flops(K, M=M_, N=N_):
@@ -310,7 +311,7 @@ def run_ours(args):
     traffic = load_traffic().get(f"gemm_bf16_8192x8192x{Kd}", {}).get("dram_bytes_per_launch")
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peaks["bf16_sustained"],
                 "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_sustained"], 4), "traffic": traffic,
-                "kernel": f"ws_gemm_tn_kernel<bf16,bf16,{512 if Kd >= 4096 else 256},cta_group::2> M=N=8192 K={Kd}",
+                "kernel": f"ws_gemm_tn_kernel<bf16,bf16,{512 if Kd >= 1024 else 256},cta_group::2> M=N=8192 K={Kd}",
                 "peak_kind": f"bf16_tflops_sustained ({peaks['source']}); the timed loop runs back to back",
                 "frac_of_burst": round(achieved / peaks["bf16"], 4),
                 "frac_of_dense_2250": round(achieved / 2250.0, 4),
@@ -332,7 +333,7 @@ def run_ours(args):
 
     settle()
     lib = {}
-    for K in ((8192, 16384) if not args.no_vs_cublas else ()):
+    for K in ((2048, 8192, 16384) if not args.no_vs_cublas else ()):
         a, b = ops[K]
         for _ in range(3):
             torch.matmul(a, b.T, out=c)
@@ -352,6 +353,25 @@ def run_ours(args):
         lib[f"bf16_8192x8192x{K}"] = {"ours_tflops": round(gemm_flops(K) / (med(ms_ours) * 1e-3) / 1e12, 1),
                                       "cublas_tflops": round(gemm_flops(K) / (med(ms_lib) * 1e-3) / 1e12, 1),
                                       "windows": "6 alternating windows of 20 launches each, medians"}
+    if not args.no_vs_cublas:
+        # the whole headline step (one pass over the K sweep) through each library, alternating
+        ms_lib, ms_ours = [], []
+        sweep = lambda f: [f(*ops[K]) for K in K_SWEEP]
+        pair = ((lambda: sweep(lambda a, b: ws.gemm_tn(a, b, c)), ms_ours),
+                (lambda: sweep(lambda a, b: torch.matmul(a, b.T, out=c)), ms_lib))
+        for w in range(6):
+            for fn, acc in (pair if w % 2 == 0 else pair[::-1]):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(3):
+                    fn()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                acc.append(e0.elapsed_time(e1) / 3)
+        med = lambda xs: sorted(xs)[len(xs) // 2]
+        lib["bf16_k_sweep_step"] = {"ours_tflops": round(STEP_FLOPS / (med(ms_ours) * 1e-3) / 1e12, 1),
+                                    "cublas_tflops": round(STEP_FLOPS / (med(ms_lib) * 1e-3) / 1e12, 1),
+                                    "windows": "6 alternating windows of 3 sweeps each (no L2 flush), medians"}
 
     # ---- attention path (C4 / C5), reported beside the headline ----
     settle()

@@ -145,6 +145,11 @@ int64_t ws_launch_count(void);
 /* Library version string, e.g. "ws-b200 0.1 sm_100a". */
 const char* ws_version(void);
 
+/* Developer diagnostics: subsequent ws_gemm_tn launches stamp %clock64 events of CTAs 0 and 1
+ * (first 32 tiles, 16 events each) into `trace`, a device buffer of 2*32*16 uint64; NULL turns
+ * it off. Event map in csrc/gemm_sm100.cuh (GT); reader: scripts/gemm_trace.py. */
+void ws_debug_gemm_trace(unsigned long long* trace);
+
 #ifdef __cplusplus
 }
 #endif

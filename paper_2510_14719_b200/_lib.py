@@ -67,6 +67,7 @@ EXPORTS = {
     "ws_gemm_tn": (ctypes.c_int, [ctypes.POINTER(GemmDesc), ctypes.c_void_p]),
     "ws_attn_fwd": (ctypes.c_int, [ctypes.POINTER(AttnDesc), ctypes.c_void_p]),
     "ws_attn_fwd_traced": (ctypes.c_int, [ctypes.POINTER(AttnDesc), ctypes.c_void_p, ctypes.c_void_p]),
+    "ws_debug_gemm_trace": (None, [ctypes.c_void_p]),
     "ws_run_kernel": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(KBuffer), ctypes.c_int32, ctypes.c_int64,
                                      ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]),
     "ws_last_error": (ctypes.c_char_p, []),

@@ -127,6 +127,8 @@ void apply_wait_hint() {
   });
 }
 
+unsigned long long* g_gemm_trace = nullptr;  // ws_debug_gemm_trace
+
 template <int IN, int OUT, int BN, int CG>
 ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   using namespace ws;
@@ -159,6 +161,8 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   if (p.group_m > p.num_m_blocks / CG) p.group_m = p.num_m_blocks / CG;
   p.scale = d.scale_a * d.scale_b;
   p.act = d.act;
+  p.trace = g_gemm_trace;
+  p.trace_global = getenv("WS_GEMM_TRACE_GLOBAL") != nullptr;
 
   CUtensorMap ta, tb, tc;
   ws_status s;
@@ -493,6 +497,8 @@ const char* ws_last_error(void) { return g_last_error.c_str(); }
 int64_t ws_launch_count(void) { return g_launches.load(); }
 const char* ws_version(void) { return "ws-b200 0.1 sm_100a"; }
 
+void ws_debug_gemm_trace(unsigned long long* trace) { g_gemm_trace = trace; }
+
 ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
   g_last_error.clear();
   if (!desc) return fail(WS_TYPE, "null descriptor");
@@ -507,10 +513,12 @@ ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
   const int eb = elem_bytes(d.in_dtype);
   if (eb == 0 || d.in_dtype == WS_F32) return fail(WS_TYPE, "in_dtype must be F16, BF16 or E4M3");
   // auto N tile: a 256 x 512 pair tile moves 25% fewer operand bytes per output than 256 x 256
-  // (what keeps the power-capped clock up on long K), but its single TMEM accumulator leaves the
-  // epilogue unoverlapped — worth it once the mainloop is >= 64 K-blocks
+  // (256 x 256 pairs are L2 -> SM bandwidth bound, ~600 instead of 512 cycles per K block); its
+  // single TMEM accumulator is handed over half by half with an early-release epilogue
   const int64_t kblocks = d.K / (128 / (eb > 0 ? eb : 1));
-  int bn = d.bn > 0 ? d.bn : (d.cta_pair && kblocks >= 64 && d.N % 512 == 0) ? 512 : 256;
+  // auto: 256 x 512 pair tiles from 16 K blocks on (bf16 K >= 1024, FP8 K >= 2048; 4-7% over
+  // 256 x 256 pairs there, equal at 8 K blocks; scripts/gemm_policy_sweep.sh), else 256-wide
+  int bn = d.bn > 0 ? d.bn : (d.cta_pair && kblocks >= 16 && d.N % 512 == 0) ? 512 : 256;
   if (bn != 128 && bn != 256 && bn != 512) return fail(WS_TYPE, "bn must be 128, 256 or 512");
   if (bn == 512 && !d.cta_pair) return fail(WS_TYPE, "bn=512 (256 x 512 tiles) needs cta_pair=1");
   const int bm = d.cta_pair ? 2 * ws::GEMM_BM : ws::GEMM_BM;

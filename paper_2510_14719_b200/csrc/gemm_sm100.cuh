@@ -40,6 +40,10 @@ struct GemmParams {
   int group_m;
   float scale;
   int act;  // 0 none, 1 relu
+  // developer diagnostics (ws_debug_gemm_trace): %clock64 stamps of CTAs 0 and 1, first 32 tiles,
+  // 16 events per tile at trace[(cta * 32 + tile) * 16 + event]; nullptr = off
+  unsigned long long* trace;
+  int trace_global;  // stamps from %globaltimer (ns, comparable across SMs) instead of %clock64
 };
 
 struct GemmSmemLayout {
@@ -95,6 +99,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   constexpr int UMMA_K_BYTES = 32;     // 16 x 16-bit or 32 x 8-bit per tcgen05.mma
   constexpr int KSTEPS = GEMM_ROW_BYTES / UMMA_K_BYTES;
   constexpr uint32_t IDESC = make_idesc(IN == IN_BF16 ? 1u : 0u, GEMM_BM * CG, MMA_N, 0, 0);
+  // 256 x 512 tiles with 16-bit output: all eight epilogue warps drain one N half at a time into
+  // registers (32 rows x 128 columns, 64 packed registers each) and release it before storing
+  constexpr bool EARLY_RELEASE = NH == 2 && OUT_BYTES == 2;
 
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -111,6 +118,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
   const bool leader = rank == 0;
   const int tile0 = static_cast<int>(blockIdx.x) / CG, tile_stride = static_cast<int>(gridDim.x) / CG;
+  unsigned long long* const trace = blockIdx.x < 2 ? p.trace : nullptr;
+#define GT(ti, ev)                                                                        \
+  do {                                                                                    \
+    if (trace && (ti) < 32)                                                               \
+      trace[(blockIdx.x * 32 + (ti)) * 16 + (ev)] = p.trace_global ? globaltimer() : clock64(); \
+  } while (0)
 
   if (warp == 0 && lane == 0) {
     tma_prefetch_desc(&tm_a);
@@ -121,7 +134,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     // the four epilogue warps of that column half; otherwise one pair per accumulator buffer
     for (int i = 0; i < (NH == 2 ? 2 : ACC); ++i) {
       mbar_init(&tmem_full[i], 1);
-      mbar_init(&tmem_empty[i], (NH == 2 ? GEMM_EPI_WARPS / 2 : GEMM_EPI_WARPS) * CG);  // per epilogue warp, per CTA
+      mbar_init(&tmem_empty[i], (NH == 2 && !EARLY_RELEASE ? GEMM_EPI_WARPS / 2 : GEMM_EPI_WARPS) * CG);  // per epilogue warp, per CTA
     }
     fence_barrier_init();
   } else if (warp == 2) {
@@ -135,18 +148,19 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
-
   if (warp == 0) {
     // ===================== TMA producer: aref put =====================
     if (lane == 0) {
       ArefCursor c;
-      for (int t = tile0; t < num_tiles; t += tile_stride) {
+      int ti = 0;
+      for (int t = tile0; t < num_tiles; t += tile_stride, ++ti) {
         int mb, nb;
         gemm_tile_coords(t, p, p.num_m_blocks / CG, mb, nb);
         const int arow = mb * GEMM_BM * CG + static_cast<int>(rank) * GEMM_BM;
         const int brow = nb * BN + static_cast<int>(rank) * B_BOX;  // + h * MMA_N for half h
         for (int kb = 0; kb < p.num_k_blocks; ++kb) {
           ring->put_acquire(c, 1);
+          if (kb == 0) GT(ti, 12);
           uint8_t* sa = smem + c.slot * L.stage_bytes;
           uint8_t* sb = sa + L.a_bytes;
           // coordinates are in elements of the tensor map's innermost dim (K) then rows
@@ -167,6 +181,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           c.advance(D);
         }
+        GT(ti, 13);
       }
     }
   } else if (warp == 1) {
@@ -211,10 +226,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         // until the epilogue has released it. The tensor core never waits for a whole epilogue.
         uint32_t pend_slot[GEMM_MAX_STAGES];
         int pend_kb[GEMM_MAX_STAGES];
-        for (int t = tile0; t < num_tiles; t += tile_stride) {
+        int ti = 0;
+        for (int t = tile0; t < num_tiles; t += tile_stride, ++ti) {
           const uint32_t par = acc_phase ^ 1u;
+          GT(ti, 0);
           mbar_wait(&tmem_empty[0], par, 3);
           tc_fence_after();
+          GT(ti, 1);
           bool h1_free = false;
           int npend = 0;
           auto flush = [&]() {
@@ -228,10 +246,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           for (int kb = 0; kb < nk; ++kb) {
             ring->get(c, 2);
             tc_fence_after();
+            if (kb == 0) GT(ti, 5);
             issue_half(c.slot, 0, kb);
             if (!h1_free && mbar_try_wait(smem_u32(&tmem_empty[1]), par)) {
               h1_free = true;
               tc_fence_after();
+              GT(ti, 2);
             }
             if ((!h1_free || kb >= tail) && npend < static_cast<int>(D) - 1) {
               pend_slot[npend] = c.slot;
@@ -241,6 +261,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
                 mbar_wait(&tmem_empty[1], par, 3);
                 tc_fence_after();
                 h1_free = true;
+                GT(ti, 2);
               }
               flush();
               issue_half(c.slot, 1, kb);
@@ -249,19 +270,25 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             c.advance(D);
           }
           commit_full(0);
+          GT(ti, 3);
           if (!h1_free) {
             mbar_wait(&tmem_empty[1], par, 3);
             tc_fence_after();
+            GT(ti, 2);
           }
           flush();
           commit_full(1);
+          GT(ti, 4);
           acc_phase ^= 1u;
         }
       } else {
-        for (int t = tile0; t < num_tiles; t += tile_stride) {
+        int ti = 0;
+        for (int t = tile0; t < num_tiles; t += tile_stride, ++ti) {
+          GT(ti, 0);
           mbar_wait(&tmem_empty[acc_stage], acc_phase ^ 1u, 3);
           if (NH == 2) mbar_wait(&tmem_empty[1], acc_phase ^ 1u, 3);
           tc_fence_after();
+          GT(ti, 1);
           for (int kb = 0; kb < p.num_k_blocks; ++kb, ++gk) {
             if (P < D && gk >= P) {
               // at most P k-blocks of MMAs in flight (ref pipeline.hpp:98-140, "wait <= P-1")
@@ -270,6 +297,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
             }
             ring->get(c, 2);
             tc_fence_after();
+            if (kb == 0) GT(ti, 5);
 #pragma unroll
             for (int h = 0; h < NH; ++h) issue_half(c.slot, h, kb);
             release(c.slot);
@@ -277,6 +305,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           commit_full(acc_stage);
           if (NH == 2) commit_full(1);
+          GT(ti, 4);
           if (++acc_stage == ACC) {
             acc_stage = 0;
             acc_phase ^= 1u;
@@ -299,68 +328,116 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       tmem_ld32(taddr, *reinterpret_cast<uint32_t(*)[32]>(&v[0]));
       if constexpr (CW == 64) tmem_ld32(taddr + 32, *reinterpret_cast<uint32_t(*)[32]>(&v[32]));
     };
-    for (int t = tile0; t < num_tiles; t += tile_stride) {
+    const bool tw = lane == 0 && q == 0;  // warps 4 (column half 0) and 8 (half 1) stamp events
+    int ti = 0;
+    for (int t = tile0; t < num_tiles; t += tile_stride, ++ti) {
       int mb, nb;
       gemm_tile_coords(t, p, p.num_m_blocks / CG, mb, nb);
       const int crow = mb * GEMM_BM * CG + static_cast<int>(rank) * GEMM_BM;
-      // BN = 512: this warp's column half is one N half with its own barrier pair
-      const int bar = NH == 2 ? hc : static_cast<int>(acc_stage);
-      mbar_wait(&tmem_full[bar], acc_phase, 5);
-      tc_fence_after();
-      const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc_stage * BN + hc * (BN / 2);
-      // one chunk: CW columns = 128 bytes of output per row
-      auto chunk = [&](uint32_t(&cur)[CW], uint32_t(&nxt)[CW], int ch) {
-        tmem_wait_ld();  // cur landed
-        if (ch + 1 < NCHW) {
-          tmem_load(t_row + (ch + 1) * CW, nxt);  // in flight while cur is converted and stored
-        } else {
-          // accumulator fully read: release it to the MMA warp (accumulator aref consumed)
-          tc_fence_before();
-          __syncwarp();
-          if (lane == 0) {
-            if constexpr (CG == 1)
-              mbar_arrive(&tmem_empty[bar]);
-            else
-              mbar_arrive_cluster(&tmem_empty[bar], 0);  // the leader's MMA warp owns the release
-          }
+      auto cvt2 = [&](uint32_t a, uint32_t b) -> uint32_t {
+        float f0 = __uint_as_float(a), f1 = __uint_as_float(b);
+        if (!plain) {
+          f0 = fmaxf(f0 * scale, lo_clamp);
+          f1 = fmaxf(f1 * scale, lo_clamp);
         }
-        uint32_t w[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if constexpr (OUT == OUT_F32) {
-            const float f = __uint_as_float(cur[j]);
-            w[j] = plain ? cur[j] : __float_as_uint(fmaxf(f * scale, lo_clamp));
-          } else {
-            float f0 = __uint_as_float(cur[2 * j]), f1 = __uint_as_float(cur[2 * j + 1]);
-            if (!plain) {
-              f0 = fmaxf(f0 * scale, lo_clamp);
-              f1 = fmaxf(f1 * scale, lo_clamp);
-            }
-            w[j] = OUT == OUT_BF16 ? pack_bf16(f0, f1) : pack_f16(f0, f1);
-          }
-        }
+        return OUT == OUT_BF16 ? pack_bf16(f0, f1) : pack_f16(f0, f1);
+      };
+      // staging of one 128-byte row chunk (8 x 16 bytes, 128B-swizzled) and its TMA store
+      auto stage_store = [&](const uint32_t* w, int col) {
         if (stores > 0) {
           if (lane == 0) tma_store_wait_read<0>();  // the previous store has read the staging buffer
           __syncwarp();
         }
-        // 8 x 16-byte chunks per row, 128B-swizzled
 #pragma unroll
         for (int j = 0; j < 8; ++j)
           st_shared_v4(row_addr + ((j ^ (lane & 7u)) << 4), w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
         fence_proxy_async_smem();
         __syncwarp();
         if (lane == 0) {
-          tma_store_2d(&tm_c, buf, nb * BN + hc * (BN / 2) + ch * CW, crow + q * 32);
+          tma_store_2d(&tm_c, buf, col, crow + q * 32);
           tma_store_commit();
         }
         ++stores;
       };
-      uint32_t va[CW], vb[CW];
-      tmem_load(t_row, va);
+      auto release_acc = [&](int bar, int ev) {  // accumulator read: release it to the MMA warp (aref consumed)
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) {
+          if (q == 0 && (EARLY_RELEASE ? hc == 0 : true)) GT(ti, ev);
+          if (EARLY_RELEASE && ev == 7 && q == 3) GT(ti, 14 + hc);  // half 0: the other warps' releases
+          if constexpr (CG == 1)
+            mbar_arrive(&tmem_empty[bar]);
+          else
+            mbar_arrive_cluster(&tmem_empty[bar], 0);  // the leader's MMA warp owns the release
+        }
+      };
+      if constexpr (EARLY_RELEASE) {
+        // half h: wait for its MMAs, load this warp's 32 rows x 128 columns (16 at a time, the next
+        // load in flight during each conversion), release the TMEM half, then stage and store. The
+        // MMA warp's next tile waits for the TMEM reads only (scripts/gemm_trace.py: with the
+        // release after the stores the tensor core idled ~5500 cycles per tile at K = 2048).
+        constexpr int HC = MMA_N / 2;  // columns per warp per half
 #pragma unroll 1
-      for (int ch = 0; ch < NCHW; ch += 2) {
-        chunk(va, vb, ch);
-        if (ch + 1 < NCHW) chunk(vb, va, ch + 1);
+        for (int h = 0; h < NH; ++h) {
+          mbar_wait(&tmem_full[h], acc_phase, 5);
+          tc_fence_after();
+          if (tw && hc == 0) GT(ti, 6 + 3 * h);
+          const uint32_t t_row = tmem_base + ((q * 32u) << 16) + h * MMA_N + hc * HC;
+          uint32_t pk[HC / 2];
+          uint32_t va[16], vb[16];
+          tmem_ld16(t_row, va);
+#pragma unroll
+          for (int i = 0; i < HC / 16; ++i) {
+            tmem_wait_ld();
+            if (i + 1 < HC / 16) {
+              if (i & 1)
+                tmem_ld16(t_row + (i + 1) * 16, va);
+              else
+                tmem_ld16(t_row + (i + 1) * 16, vb);
+            }
+            const uint32_t* cur = (i & 1) ? vb : va;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pk[i * 8 + j] = cvt2(cur[2 * j], cur[2 * j + 1]);
+          }
+          release_acc(h, 7 + 3 * h);
+#pragma unroll
+          for (int ch = 0; ch < HC / CW; ++ch) stage_store(pk + ch * 32, nb * BN + h * MMA_N + hc * HC + ch * CW);
+          if (tw && hc == 0) GT(ti, 8 + 3 * h);
+        }
+      } else {
+        // BN = 512: this warp's column half is one N half with its own barrier pair
+        const int bar = NH == 2 ? hc : static_cast<int>(acc_stage);
+        mbar_wait(&tmem_full[bar], acc_phase, 5);
+        tc_fence_after();
+        if (tw) GT(ti, 6 + 3 * hc);
+        const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc_stage * BN + hc * (BN / 2);
+        // one chunk: CW columns = 128 bytes of output per row
+        auto chunk = [&](uint32_t(&cur)[CW], uint32_t(&nxt)[CW], int ch) {
+          tmem_wait_ld();  // cur landed
+          if (ch + 1 < NCHW)
+            tmem_load(t_row + (ch + 1) * CW, nxt);  // in flight while cur is converted and stored
+          else
+            release_acc(bar, 7 + 3 * hc);
+          uint32_t w[32];
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            if constexpr (OUT == OUT_F32) {
+              const float f = __uint_as_float(cur[j]);
+              w[j] = plain ? cur[j] : __float_as_uint(fmaxf(f * scale, lo_clamp));
+            } else {
+              w[j] = cvt2(cur[2 * j], cur[2 * j + 1]);
+            }
+          }
+          stage_store(w, nb * BN + hc * (BN / 2) + ch * CW);
+        };
+        uint32_t va[CW], vb[CW];
+        tmem_load(t_row, va);
+#pragma unroll 1
+        for (int ch = 0; ch < NCHW; ch += 2) {
+          chunk(va, vb, ch);
+          if (ch + 1 < NCHW) chunk(vb, va, ch + 1);
+        }
+        if (tw) GT(ti, 8 + 3 * hc);
       }
       if (++acc_stage == ACC) {
         acc_stage = 0;
@@ -379,6 +456,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, TMEM_COLS);
   }
+#undef GT
 }
 
 }  // namespace ws

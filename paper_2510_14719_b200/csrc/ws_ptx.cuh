@@ -69,7 +69,7 @@ __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta)
   asm volatile(
       "{\n\t.reg .b32 remAddr32;\n\t"
       "mapa.shared::cluster.u32  remAddr32, %0, %1;\n\t"
-      "mbarrier.arrive.release.cluster.shared::cluster.b64  _, [remAddr32];\n\t}" ::"r"(smem_u32(bar)),
+      "mbarrier.arrive.shared::cluster.b64  _, [remAddr32];\n\t}" ::"r"(smem_u32(bar)),
       "r"(cta)
       : "memory");
 }

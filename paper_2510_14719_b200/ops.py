@@ -38,8 +38,8 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
 
     a, b: row-major (last dim contiguous) CUDA tensors of dtype f16/bf16/float8_e4m3fn.
     out: optional [M,N] tensor (may be a column slice of a wider matrix; its row stride is ldc).
-    cta_pair: None = auto (cta_group::2 CTA pairs when M % 256 == 0 and K >= 512, where the
-    mainloop dominates; single-CTA tiles for shorter K, where the epilogue does).
+    cta_pair: None = auto (cta_group::2 CTA pairs when M % 256 == 0 and K >= 256; single-CTA
+    128 x 256 tiles otherwise).
     bn: 0 = auto (the library picks 256 x 512 pair tiles for long K, else 256-wide tiles).
     """
     if a.device.type != "cuda" or b.device.type != "cuda":
@@ -53,7 +53,7 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
     if a.stride(1) != 1 or b.stride(1) != 1:
         raise _lib.WsError(2, "operands must be K-contiguous (row-major)")
     if cta_pair is None:
-        cta_pair = M % 256 == 0 and K >= 512
+        cta_pair = M % 256 == 0 and K >= 256
     if out is None:
         od = out_dtype or (torch.bfloat16 if a.dtype == torch.float8_e4m3fn else a.dtype)
         out = torch.empty((M, N), dtype=od, device=a.device)

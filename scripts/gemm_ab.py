@@ -50,7 +50,10 @@ secs = float(os.environ.get("SECS", "1.0"))
 res = {i: [] for i in range(len(cfgs))}
 for r in range(int(os.environ.get("ROUNDS", "3"))):
     for i, cfg in enumerate(cfgs):
-        if cfg.get("cublas"):
+        if cfg.get("cublas") and dt == torch.float8_e4m3fn:
+            one = torch.ones((), device="cuda")  # cuBLASLt FP8 through torch._scaled_mm (per-tensor scales)
+            fn = lambda one=one: torch._scaled_mm(a, b.T, one, one, out_dtype=torch.bfloat16, out=c)
+        elif cfg.get("cublas"):
             fn = lambda: torch.matmul(a, b.T, out=c)
         else:
             fn = lambda cfg=cfg: ws.gemm_tn(a, b, c, **cfg)

@@ -184,3 +184,34 @@ def test_pair_512_tiles_pipeline_depths(ws, dev, D, P):
     M, N, K = 2048, 8192, 320  # 128 tiles (~2 per CTA pair), 5 K blocks
     _, _, c = _run(ws, dev, M, N, K, BF16, F32, cta_pair=True, bn=512, D=D, P=P, persistent=True)
     assert np.array_equal(as_f64(c), _want(M, N, K))
+
+
+@pytest.mark.parametrize("out_dt", [BF16, F16])
+@pytest.mark.parametrize("K,kw", [(128, dict(D=4)), (1024, {}), (2048, dict(D=3)), (4096, dict(scale_a=0.5))])
+def test_pair_512_16bit_out_equals_rounded_oracle(ws, dev, out_dt, K, kw):
+    """256 x 512 pair tiles with 16-bit output (the early-release epilogue: all eight epilogue
+    warps drain one N half into registers, release it, then store). The fp32 accumulation is exact
+    for the reference payloads, so the output must equal the oracle rounded once to out_dt."""
+    M, N = 1024, 4096  # 32 pair tiles (fewer than the 74 pairs), then 64 at 2048 rows
+    for m in (M, 2048):
+        a = ref_tensor("a", (m, K), BF16, dev)
+        b = ref_tensor("b", (N, K), BF16, dev)
+        c = ws.gemm_tn(a, b, out_dtype=out_dt, cta_pair=True, bn=512, **kw)
+        torch.cuda.synchronize()
+        scale = kw.get("scale_a", 1.0)
+        want = torch.from_numpy(_want(m, N, K, scale=scale)).to(dev).to(out_dt)
+        assert torch.equal(c, want), (m, K, kw)
+
+
+def test_pair_512_many_tiles_per_pair_16bit(ws, dev):
+    """~14 tiles per CTA pair (8192 x 8192 with 256 x 512 tiles): every hand-over of both N halves
+    between the MMA warp and the early-release epilogue, sampled rows exact after rounding."""
+    M = N = 8192
+    K = 512
+    a = ref_tensor("a", (M, K), BF16, dev)
+    b = ref_tensor("b", (N, K), BF16, dev)
+    c = ws.gemm_tn(a, b, out_dtype=BF16, cta_pair=True, bn=512)
+    torch.cuda.synchronize()
+    rows = np.array([0, 255, 256, 4095, 4096, 8191] + list(np.random.default_rng(7).integers(0, M, 10)))
+    want = torch.from_numpy(_want(M, N, K, rows=rows)).to(dev).to(BF16)
+    assert torch.equal(c[torch.from_numpy(rows).to(dev)], want)
