@@ -10,6 +10,11 @@ slot (i % 2); events order every reuse:
   GEMM(i)  waits H2D(i), D2H(i-2)   (inputs landed; its C slot has been copied out)
   D2H(i)   waits GEMM(i)
 Slot events persist across calls, so consecutive calls keep the pipeline full.
+
+Large jobs are also split into row chunks (A rows, C rows; B is copied once per job): the GEMM of
+chunk j starts when its A rows have landed and its C rows leave as soon as it is done, so the
+pipeline's tail — the last job's GEMM plus its whole C copy-out, during which the host->device
+direction idles — shrinks to one chunk (scripts/e2e_probe.py).
 """
 from __future__ import annotations
 
@@ -43,11 +48,24 @@ class _Pipe:
 _pipes: Dict[int, _Pipe] = {}
 
 
+def _row_chunks(M: int, c_bytes: int, row_chunks: Optional[int]) -> int:
+    if row_chunks is not None:
+        n = max(1, int(row_chunks))
+    else:
+        n = max(1, round(c_bytes / (32 << 20)))  # ~32 MB of C per chunk
+    # every chunk a whole number of 256-row CTA-pair blocks
+    while n > 1 and (M % n or (M // n) % 256):
+        n -= 1
+    return n
+
+
 def gemm_tn_host(jobs: Sequence[Tuple[torch.Tensor, torch.Tensor, torch.Tensor]], *,
-                 device: Optional[torch.device] = None, **gemm_kw) -> torch.cuda.Event:
+                 device: Optional[torch.device] = None, row_chunks: Optional[int] = None,
+                 **gemm_kw) -> torch.cuda.Event:
     """Run c = a . b^T for every (a, b, c) in `jobs`: a [M,K], b [N,K], c [M,N] host tensors
     (pinned for asynchronous copies). Returns a CUDA event that completes when every c is in host
-    memory; the caller's current stream is made to wait on it. gemm_kw: ws.gemm_tn knobs."""
+    memory; the caller's current stream is made to wait on it. row_chunks: pieces each job's rows
+    are split into (None = auto, ~32 MB of C each). gemm_kw: ws.gemm_tn knobs."""
     dev = device or torch.device("cuda", torch.cuda.current_device())
     if dev.type != "cuda":
         raise _lib.WsError(2, "gemm_tn_host needs a CUDA device (no CPU path)")
@@ -68,28 +86,34 @@ def gemm_tn_host(jobs: Sequence[Tuple[torch.Tensor, torch.Tensor, torch.Tensor]]
         da = p.buf(("a", slot), a.shape, a.dtype)
         db = p.buf(("b", slot), b.shape, b.dtype)
         dc = p.buf(("c", slot), c.shape, c.dtype)
-        # H2D(i) after GEMM(i-2) has read the slot
+        M = a.shape[0]
+        n = _row_chunks(M, c.numel() * c.element_size(), row_chunks)
+        rows = M // n
+        # H2D(i) after every GEMM of job i-2 has read the slot
         if p.gemm_done[slot] is not None:
             p.s_h2d.wait_event(p.gemm_done[slot])
-        with torch.cuda.stream(p.s_h2d):
-            da.copy_(a, non_blocking=True)
-            db.copy_(b, non_blocking=True)
-            h2d = torch.cuda.Event()
-            h2d.record(p.s_h2d)
-        # GEMM(i) after its inputs landed and D2H(i-2) has copied the C slot out
-        p.s_comp.wait_event(h2d)
+        # GEMMs of job i after D2H(i-2) has copied the C slot out
         if p.d2h_done[slot] is not None:
             p.s_comp.wait_event(p.d2h_done[slot])
-        gemm_tn(da, db, dc, stream=p.s_comp, **gemm_kw)
-        g = torch.cuda.Event()
-        g.record(p.s_comp)
+        with torch.cuda.stream(p.s_h2d):
+            db.copy_(b, non_blocking=True)
+        g = d = None
+        for j in range(n):
+            r = slice(j * rows, (j + 1) * rows)
+            with torch.cuda.stream(p.s_h2d):
+                da[r].copy_(a[r], non_blocking=True)
+                h2d = torch.cuda.Event()
+                h2d.record(p.s_h2d)
+            p.s_comp.wait_event(h2d)
+            gemm_tn(da[r], db, dc[r], stream=p.s_comp, **gemm_kw)
+            g = torch.cuda.Event()
+            g.record(p.s_comp)
+            p.s_d2h.wait_event(g)
+            with torch.cuda.stream(p.s_d2h):
+                c[r].copy_(dc[r], non_blocking=True)
+                d = torch.cuda.Event()
+                d.record(p.s_d2h)
         p.gemm_done[slot] = g
-        # D2H(i) after GEMM(i)
-        p.s_d2h.wait_event(g)
-        with torch.cuda.stream(p.s_d2h):
-            c.copy_(dc, non_blocking=True)
-            d = torch.cuda.Event()
-            d.record(p.s_d2h)
         p.d2h_done[slot] = d
         last = d
     done = torch.cuda.Event()

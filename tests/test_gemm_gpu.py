@@ -156,10 +156,12 @@ def test_launches_are_counted(ws, dev):
     assert ws.launch_count() == n0 + 1
 
 
-def test_host_pipeline_matches_device_path_bit_exact(ws, dev):
+@pytest.mark.parametrize("row_chunks", [None, 2, 4])
+def test_host_pipeline_matches_device_path_bit_exact(ws, dev, row_chunks):
     """gemm_tn_host (host buffers, H2D / GEMM / D2H overlapped on three streams, slots reused every
-    other job) gives the oracle's exact fp32 results for every job, across two calls."""
-    shapes = [(256, 512, 128), (512, 256, 1024), (256, 256, 64), (512, 512, 256), (256, 768, 512)]
+    other job, jobs split into 256-row chunks where row_chunks asks and M allows) gives the oracle's
+    exact fp32 results for every job, across two calls."""
+    shapes = [(256, 512, 128), (512, 256, 1024), (256, 256, 64), (1024, 512, 256), (768, 768, 512)]
     jobs, want = [], []
     for i, (M, N, K) in enumerate(shapes):
         a = oracle.generate_real(f"a{i}", (M, K))
@@ -171,7 +173,7 @@ def test_host_pipeline_matches_device_path_bit_exact(ws, dev):
     for _ in range(2):
         for _, _, c in jobs:
             c.fill_(float("nan"))
-        ev = ws.gemm_tn_host(jobs, device=dev)
+        ev = ws.gemm_tn_host(jobs, device=dev, row_chunks=row_chunks)
         ev.synchronize()
         for (_, _, c), w in zip(jobs, want):
             assert np.array_equal(c.numpy().astype(np.float64), w)
