@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <string>
 
 #include "../../include/ws.h"
@@ -113,6 +114,19 @@ int num_sms() {
 
 constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA on sm_100a
 
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size (it costs a driver
+// call per launch otherwise; small GEMMs are launch-bound)
+cudaError_t allow_smem(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::unordered_map<const void*, int> done;
+  std::lock_guard<std::mutex> g(mu);
+  auto it = done.find(kern);
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done[kern] = bytes;
+  return e;
+}
+
 // Suspend-time hint of blocked mbarrier waits in this module's kernels: a waiting warp sleeps in
 // the barrier (woken when the phase completes) instead of re-issuing try_wait, which leaves the
 // issue slots to the softmax warps sharing its SM sub-partition (hdim-64 causal attention +5-10%,
@@ -175,7 +189,7 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   if ((s = make_tmap(&tc, d.C, out_dt, d.M, d.N, d.ldc, 32, cw, CU_TENSOR_MAP_L2_PROMOTION_NONE)) != WS_OK) return s;
 
   auto kern = ws_gemm_tn_kernel<IN, OUT, BN, CG>;
-  WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)L.total));
+  WS_CUDA_CHECK(allow_smem(reinterpret_cast<const void*>(kern), (int)L.total));
   const int tiles = (p.num_m_blocks / CG) * p.num_n_blocks;
   const int units = num_sms() / CG;  // persistent: one CTA (pair) per SM (pair)
   int grid = CG * (d.persistent ? (tiles < units ? tiles : units) : tiles);
@@ -269,7 +283,7 @@ ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stre
   if ((s = make_tmap(&tk, d.K, dt, rows, DH, DH, ATTN_BN, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
   if ((s = make_tmap(&tv, d.V, dt, rows, DH, DH, ATTN_BN, 64, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK) return s;
   auto kern = ws_attn_fwd_kernel<DH, BF16>;
-  WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  WS_CUDA_CHECK(allow_smem(reinterpret_cast<const void*>(kern), (int)smem));
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(bh1 - bh0, p.num_pairs);
   cfg.blockDim = dim3(ATTN_THREADS);
@@ -344,7 +358,7 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
       default: break;
     }
   }
-  WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  WS_CUDA_CHECK(allow_smem(reinterpret_cast<const void*>(kern), (int)smem));
   cudaLaunchConfig_t cfg = {};
   {
     // persistent: one CTA per SM over the (pair, (b,h)) items (both 128-key kernels);
@@ -426,7 +440,7 @@ ws_status launch_attn_fp8(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t 
       default: break;
     }
   }
-  WS_CUDA_CHECK(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  WS_CUDA_CHECK(allow_smem(reinterpret_cast<const void*>(kern), (int)smem));
   cudaLaunchConfig_t cfg = {};
   const int items = p.num_pairs * p.num_bh;
   cfg.gridDim = dim3(items < num_sms() ? items : num_sms());
@@ -518,7 +532,15 @@ ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
   const int64_t kblocks = d.K / (128 / (eb > 0 ? eb : 1));
   // auto: 256 x 512 pair tiles from 16 K blocks on (bf16 K >= 1024, FP8 K >= 2048; 4-7% over
   // 256 x 256 pairs there, equal at 8 K blocks; scripts/gemm_policy_sweep.sh), else 256-wide
-  int bn = d.bn > 0 ? d.bn : (d.cta_pair && kblocks >= 16 && d.N % 512 == 0) ? 512 : 256;
+  // ... and only when the grid still fills the GPU: small problems take the smaller tile with
+  // more work units (1024^3: 128 x 128 single-CTA tiles, 64 CTAs)
+  const int64_t units = num_sms();
+  const bool fill512 = (d.M / 256) * (d.N / 512) >= units / 2;
+  const bool fill256 = (d.M / 128) * (d.N / 256) >= units;
+  int bn = d.bn > 0 ? d.bn
+           : (d.cta_pair && kblocks >= 16 && d.N % 512 == 0 && fill512) ? 512
+           : (!d.cta_pair && !fill256 && d.N % 128 == 0)                 ? 128
+                                                                         : 256;
   if (bn != 128 && bn != 256 && bn != 512) return fail(WS_TYPE, "bn must be 128, 256 or 512");
   if (bn == 512 && !d.cta_pair) return fail(WS_TYPE, "bn=512 (256 x 512 tiles) needs cta_pair=1");
   const int bm = d.cta_pair ? 2 * ws::GEMM_BM : ws::GEMM_BM;

@@ -30,6 +30,16 @@ def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
     return s.cuda_stream
 
 
+_SMS: dict = {}
+
+
+def _sm_count(device: torch.device) -> int:
+    idx = device.index if device.index is not None else torch.cuda.current_device()
+    if idx not in _SMS:
+        _SMS[idx] = torch.cuda.get_device_properties(idx).multi_processor_count
+    return _SMS[idx]
+
+
 def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None, *,
             out_dtype: Optional[torch.dtype] = None, scale_a: float = 1.0, scale_b: float = 1.0,
             D: int = 0, P: int = 0, persistent: bool = True, cta_pair: Optional[bool] = None, bn: int = 0,
@@ -38,8 +48,8 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
 
     a, b: row-major (last dim contiguous) CUDA tensors of dtype f16/bf16/float8_e4m3fn.
     out: optional [M,N] tensor (may be a column slice of a wider matrix; its row stride is ldc).
-    cta_pair: None = auto (cta_group::2 CTA pairs when M % 256 == 0 and K >= 256; single-CTA
-    128 x 256 tiles otherwise).
+    cta_pair: None = auto (cta_group::2 CTA pairs when M % 256 == 0, K >= 256 and the pair tiles
+    fill the GPU; single-CTA tiles otherwise).
     bn: 0 = auto (the library picks 256 x 512 pair tiles for long K, else 256-wide tiles).
     """
     if a.device.type != "cuda" or b.device.type != "cuda":
@@ -53,7 +63,8 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
     if a.stride(1) != 1 or b.stride(1) != 1:
         raise _lib.WsError(2, "operands must be K-contiguous (row-major)")
     if cta_pair is None:
-        cta_pair = M % 256 == 0 and K >= 256
+        # pairs only when the 256 x 256 pair tiles still give every SM pair a tile
+        cta_pair = M % 256 == 0 and K >= 256 and (M // 256) * (N // 256) >= _sm_count(a.device) // 2
     if out is None:
         od = out_dtype or (torch.bfloat16 if a.dtype == torch.float8_e4m3fn else a.dtype)
         out = torch.empty((M, N), dtype=od, device=a.device)
