@@ -85,8 +85,43 @@ CUtensorMapDataType tma_dtype(int dt) {
 
 // 2-D row-major tensor [rows x cols] with row stride `ld` elements; box [box_rows x box_cols];
 // 128-byte swizzle (box_cols * elem == 128).
+ws_status make_tmap_uncached(CUtensorMap* m, const void* ptr, int dt, int64_t rows, int64_t cols, int64_t ld,
+                             uint32_t box_rows, uint32_t box_cols, CUtensorMapL2promotion promo);
+
+// Tensor maps only encode address, shape, strides and box, so a map built for the same operand
+// is reused (per host thread, 32 entries, round robin): repeated calls on the same buffers skip
+// the driver encode (small GEMMs are host-bound; scripts/host_overhead.py)
 ws_status make_tmap(CUtensorMap* m, const void* ptr, int dt, int64_t rows, int64_t cols, int64_t ld,
                     uint32_t box_rows, uint32_t box_cols, CUtensorMapL2promotion promo) {
+  struct Entry {
+    const void* ptr;
+    int dt;
+    int64_t rows, cols, ld;
+    uint32_t br, bc;
+    int promo;
+    CUtensorMap map;
+  };
+  thread_local Entry cache[32];
+  thread_local int n = 0, next = 0;
+  for (int i = 0; i < n; ++i) {
+    const Entry& e = cache[i];
+    if (e.ptr == ptr && e.dt == dt && e.rows == rows && e.cols == cols && e.ld == ld && e.br == box_rows &&
+        e.bc == box_cols && e.promo == static_cast<int>(promo)) {
+      *m = e.map;
+      return WS_OK;
+    }
+  }
+  const ws_status s = make_tmap_uncached(m, ptr, dt, rows, cols, ld, box_rows, box_cols, promo);
+  if (s != WS_OK) return s;
+  Entry& e = cache[next];
+  e = Entry{ptr, dt, rows, cols, ld, box_rows, box_cols, static_cast<int>(promo), *m};
+  next = (next + 1) % 32;
+  if (n < 32) ++n;
+  return WS_OK;
+}
+
+ws_status make_tmap_uncached(CUtensorMap* m, const void* ptr, int dt, int64_t rows, int64_t cols, int64_t ld,
+                             uint32_t box_rows, uint32_t box_cols, CUtensorMapL2promotion promo) {
   auto enc = get_encode();
   if (!enc) return fail(WS_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable (driver too old?)");
   const int eb = elem_bytes(dt);

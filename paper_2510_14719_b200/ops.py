@@ -25,12 +25,15 @@ _DT = {torch.float32: _lib.WS_F32, torch.float16: _lib.WS_F16, torch.bfloat16: _
        torch.float8_e4m3fn: _lib.WS_E4M3}
 
 
-def _stream_ptr(stream: Optional[torch.cuda.Stream]) -> int:
-    s = stream if stream is not None else torch.cuda.current_stream()
-    return s.cuda_stream
+def _stream_ptr(stream: Optional[torch.cuda.Stream], device: Optional[torch.device] = None) -> int:
+    if stream is not None:
+        return stream.cuda_stream
+    idx = device.index if device is not None and device.index is not None else torch.cuda.current_device()
+    return torch._C._cuda_getCurrentRawStream(idx)  # the current stream's handle, without a Stream object
 
 
 _SMS: dict = {}
+_DESC_CACHE: dict = {}
 
 
 def _sm_count(device: torch.device) -> int:
@@ -70,18 +73,27 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
         out = torch.empty((M, N), dtype=od, device=a.device)
     if out.stride(1) != 1 or tuple(out.shape) != (M, N):
         raise _lib.WsError(2, "out must be [M, N] with contiguous rows")
-    d = _lib.GemmDesc()
-    d.in_dtype = _DT[a.dtype]
-    d.out_dtype = _DT[out.dtype]
-    d.M, d.N, d.K = M, N, K
-    d.A, d.lda = a.data_ptr(), a.stride(0)
-    d.B, d.ldb = b.data_ptr(), b.stride(0)
-    d.C, d.ldc = out.data_ptr(), out.stride(0)
-    d.scale_a, d.scale_b = scale_a, scale_b
-    d.D, d.P = D, P
-    d.persistent, d.cta_pair, d.bn, d.group_m = int(persistent), int(cta_pair), bn, group_m
+    # descriptors are reused for repeated calls on the same buffers and knobs (host cost per call
+    # matters for small GEMMs; scripts/host_overhead.py)
+    key = (a.data_ptr(), b.data_ptr(), out.data_ptr(), M, N, K, a.stride(0), b.stride(0), out.stride(0),
+           a.dtype, out.dtype, scale_a, scale_b, D, P, persistent, cta_pair, bn, group_m)
+    d = _DESC_CACHE.get(key)
+    if d is None:
+        d = _lib.GemmDesc()
+        d.in_dtype = _DT[a.dtype]
+        d.out_dtype = _DT[out.dtype]
+        d.M, d.N, d.K = M, N, K
+        d.A, d.lda = a.data_ptr(), a.stride(0)
+        d.B, d.ldb = b.data_ptr(), b.stride(0)
+        d.C, d.ldc = out.data_ptr(), out.stride(0)
+        d.scale_a, d.scale_b = scale_a, scale_b
+        d.D, d.P = D, P
+        d.persistent, d.cta_pair, d.bn, d.group_m = int(persistent), int(cta_pair), bn, group_m
+        if len(_DESC_CACHE) >= 64:
+            _DESC_CACHE.clear()
+        _DESC_CACHE[key] = d
     lib = _lib.load()
-    _lib.check(lib.ws_gemm_tn(ctypes.byref(d), ctypes.c_void_p(_stream_ptr(stream))))
+    _lib.check(lib.ws_gemm_tn(ctypes.byref(d), _stream_ptr(stream, a.device)))
     return out
 
 
