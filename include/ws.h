@@ -145,6 +145,23 @@ int64_t ws_launch_count(void);
 /* Library version string, e.g. "ws-b200 0.1 sm_100a". */
 const char* ws_version(void);
 
+/* Device watchdog (the simulator's Deadlock verdict, ref proj/include/warpspec/sim.hpp:49-54,
+ * 112-115, on hardware): every mbarrier wait in the kernels traps after 4 s without progress;
+ * the first waiter to time out records where it waited in pinned host memory, so the record is
+ * readable after the trap has torn down the CUDA context. */
+typedef struct ws_watchdog_info {
+  int32_t fired;     /* 1: a wait timed out and the kernel trapped */
+  uint32_t block_x;  /* CTA of the waiter */
+  uint32_t block_y;
+  uint32_t thread;   /* threadIdx.x of the waiter (warp = thread / 32: its role) */
+  uint32_t barrier;  /* shared-memory address of the mbarrier */
+  uint32_t parity;   /* phase parity it waited for */
+  uint32_t tag;      /* wait site (aref put/get, accumulator, softmax, ...; trace.py TAGS) */
+} ws_watchdog_info;
+
+/* Returns 1 and fills `out` if a watchdog fired in this process, else 0. */
+int32_t ws_watchdog(ws_watchdog_info* out);
+
 /* Developer diagnostics: subsequent ws_gemm_tn launches stamp %clock64 events of CTAs 0 and 1
  * (first 32 tiles, 16 events each) into `trace`, a device buffer of 2*32*16 uint64; NULL turns
  * it off. Event map in csrc/gemm_sm100.cuh (GT); reader: scripts/gemm_trace.py. */

@@ -63,17 +63,28 @@ class KBuffer(ctypes.Structure):
 
 
 # every symbol include/ws.h declares, with its ctypes signature
+class WatchdogInfo(ctypes.Structure):
+    """Mirror of ws_watchdog_info (include/ws.h)."""
+    _fields_ = [("fired", ctypes.c_int32), ("block_x", ctypes.c_uint32), ("block_y", ctypes.c_uint32),
+                ("thread", ctypes.c_uint32), ("barrier", ctypes.c_uint32), ("parity", ctypes.c_uint32),
+                ("tag", ctypes.c_uint32)]
+
+
 EXPORTS = {
     "ws_gemm_tn": (ctypes.c_int, [ctypes.POINTER(GemmDesc), ctypes.c_void_p]),
     "ws_attn_fwd": (ctypes.c_int, [ctypes.POINTER(AttnDesc), ctypes.c_void_p]),
     "ws_attn_fwd_traced": (ctypes.c_int, [ctypes.POINTER(AttnDesc), ctypes.c_void_p, ctypes.c_void_p]),
     "ws_debug_gemm_trace": (None, [ctypes.c_void_p]),
+    "ws_watchdog": (ctypes.c_int32, [ctypes.c_void_p]),
     "ws_run_kernel": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(KBuffer), ctypes.c_int32, ctypes.c_int64,
                                      ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]),
     "ws_last_error": (ctypes.c_char_p, []),
     "ws_launch_count": (ctypes.c_int64, []),
     "ws_version": (ctypes.c_char_p, []),
 }
+
+
+OPTIONAL = {"ws_debug_gemm_trace", "ws_watchdog"}
 
 
 class WsError(RuntimeError):
@@ -97,6 +108,8 @@ def load(path: str = LIB_PATH) -> ctypes.CDLL:
                 "There is no CPU fallback on this path.")
         lib = ctypes.CDLL(path)
         for name, (res, args) in EXPORTS.items():
+            if name in OPTIONAL and not hasattr(lib, name):
+                continue  # diagnostics absent from an older build selected with WS_LIB
             fn = getattr(lib, name)
             fn.restype = res
             fn.argtypes = args

@@ -167,12 +167,26 @@ cudaError_t allow_smem(const void* kern, int bytes) {
 // issue slots to the softmax warps sharing its SM sub-partition (hdim-64 causal attention +5-10%,
 // GEMM unchanged; scripts/attn_ab.py). WS_WAIT_HINT_NS overrides (0 = hardware default). Set once
 // per device context before the first launch.
+ws::WatchdogRecord* g_watchdog_host = nullptr;  // pinned, mapped: survives a trapped context
+
 void apply_wait_hint() {
   static std::once_flag once;
   std::call_once(once, [] {
     const char* e = getenv("WS_WAIT_HINT_NS");
     const uint32_t ns = e ? static_cast<uint32_t>(atoi(e)) : 200000u;
     cudaMemcpyToSymbol(ws::ws_wait_hint_ns, &ns, sizeof(ns));
+    // the watchdog's host-mapped record (ws_watchdog)
+    void* h = nullptr;
+    cudaError_t e1 = cudaHostAlloc(&h, sizeof(ws::WatchdogRecord), cudaHostAllocMapped), e2 = cudaErrorUnknown,
+                e3 = cudaErrorUnknown;
+    void* d = nullptr;
+    if (e1 == cudaSuccess) {
+      std::memset(h, 0, sizeof(ws::WatchdogRecord));
+      e2 = cudaHostGetDevicePointer(&d, h, 0);
+      if (e2 == cudaSuccess) e3 = cudaMemcpyToSymbol(ws::ws_watchdog_host, &d, sizeof(d));
+      if (e3 == cudaSuccess) g_watchdog_host = static_cast<ws::WatchdogRecord*>(h);
+    }
+
   });
 }
 
@@ -211,6 +225,10 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   p.scale = d.scale_a * d.scale_b;
   p.act = d.act;
   p.trace = g_gemm_trace;
+  // developer diagnostics: WS_DEBUG_DEADLOCK=1 makes CTA 0's producer skip its first aref put, so
+  // the MMA warp waits forever and the watchdog fires (the simulator's Deadlock verdict on hardware)
+  static const int deadlock_env = getenv("WS_DEBUG_DEADLOCK") ? atoi(getenv("WS_DEBUG_DEADLOCK")) : 0;
+  p.debug_deadlock = deadlock_env;
   p.trace_global = getenv("WS_GEMM_TRACE_GLOBAL") != nullptr;
 
   CUtensorMap ta, tb, tc;
@@ -547,6 +565,22 @@ int64_t ws_launch_count(void) { return g_launches.load(); }
 const char* ws_version(void) { return "ws-b200 0.1 sm_100a"; }
 
 void ws_debug_gemm_trace(unsigned long long* trace) { g_gemm_trace = trace; }
+
+int32_t ws_watchdog(ws_watchdog_info* out) {
+  const volatile ws::WatchdogRecord* r = g_watchdog_host;
+  if (out) std::memset(out, 0, sizeof(*out));
+  if (r == nullptr || r->fired != 1u) return 0;
+  if (out) {
+    out->fired = 1;
+    out->block_x = static_cast<uint32_t>(r->block & 0xffffffffu);
+    out->block_y = static_cast<uint32_t>(r->block >> 32);
+    out->thread = r->thread;
+    out->barrier = r->bar_smem;
+    out->parity = r->parity;
+    out->tag = r->tag;
+  }
+  return 1;
+}
 
 ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
   g_last_error.clear();

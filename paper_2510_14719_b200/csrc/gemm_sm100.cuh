@@ -44,6 +44,7 @@ struct GemmParams {
   // 16 events per tile at trace[(cta * 32 + tile) * 16 + event]; nullptr = off
   unsigned long long* trace;
   int trace_global;  // stamps from %globaltimer (ns, comparable across SMs) instead of %clock64
+  int debug_deadlock;  // WS_DEBUG_DEADLOCK: CTA 0 skips its first put (watchdog demonstration)
 };
 
 struct GemmSmemLayout {
@@ -161,6 +162,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         for (int kb = 0; kb < p.num_k_blocks; ++kb) {
           ring->put_acquire(c, 1);
           if (kb == 0) GT(ti, 12);
+          if (p.debug_deadlock && blockIdx.x == 0 && ti == 0 && kb == 0) {  // never staged
+            c.advance(D);
+            continue;
+          }
           uint8_t* sa = smem + c.slot * L.stage_bytes;
           uint8_t* sb = sa + L.a_bytes;
           // coordinates are in elements of the tensor map's innermost dim (K) then rows

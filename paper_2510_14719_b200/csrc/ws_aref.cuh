@@ -27,25 +27,55 @@
 namespace ws {
 
 static __device__ WatchdogRecord ws_watchdog_record;
+// host-mapped copy (pinned, zero-copy; set by the host launcher): readable after the trap has
+// torn down the context, which is how ws_watchdog() reports the Deadlock verdict
+static __device__ WatchdogRecord* ws_watchdog_host;
 // suspend-time hint (ns) for blocked waits; 0 = the hardware default (set by the host launcher)
 static __device__ uint32_t ws_wait_hint_ns;
 
-// Out of line on purpose would force ABI register saves in the 224-register softmax regions
-// (setmaxnreg budgets are per region); the slow path is inlined and stays cold.
+// The watchdog's report, out of line and noreturn: no caller state survives a trap, so the call
+// costs the wait sites nothing (an inline version that could fall back into the wait loop slowed
+// the hdim-128 attention kernel by 14%). The first waiter to time out (elected in device memory)
+// records where it waited — in the device record and in the host-mapped copy, which survives the
+// trap — and the others hold their trap until it has (a trap ends every thread of the grid).
+[[noreturn]] static __device__ __noinline__ void ws_watchdog_fire(uint32_t bar, uint32_t parity, uint32_t tag) {
+  if (atomicCAS(&ws_watchdog_record.fired, 0u, 1u) == 0u) {
+    const unsigned long long blk = blockIdx.x | (static_cast<unsigned long long>(blockIdx.y) << 32);
+    ws_watchdog_record.block = blk;
+    ws_watchdog_record.thread = threadIdx.x;
+    ws_watchdog_record.bar_smem = bar;
+    ws_watchdog_record.parity = parity;
+    ws_watchdog_record.tag = tag;
+    volatile WatchdogRecord* v = *reinterpret_cast<WatchdogRecord* volatile*>(&ws_watchdog_host);
+    if (v != nullptr) {
+      v->block = blk;
+      v->thread = threadIdx.x;
+      v->bar_smem = bar;
+      v->parity = parity;
+      v->tag = tag;
+      __threadfence_system();
+      v->fired = 1u;
+    }
+    __threadfence_system();
+    atomicExch(&ws_watchdog_record.fired, 2u);
+  } else {
+    const uint64_t t1 = globaltimer();
+    while (*reinterpret_cast<volatile unsigned int*>(&ws_watchdog_record.fired) != 2u &&
+           globaltimer() - t1 < 100000000ull) {
+    }
+  }
+  __threadfence_system();
+  asm volatile("trap;");
+  __builtin_unreachable();
+}
+
 static __device__ __forceinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity, uint32_t tag) {
   uint64_t t0 = globaltimer();
   uint32_t spins = 0;
-  const uint32_t hint = ws_wait_hint_ns;
+  // volatile load: written only by the host (cudaMemcpyToSymbol), never folded to its initialiser
+  const uint32_t hint = *reinterpret_cast<volatile uint32_t*>(&ws_wait_hint_ns);
   while (!(hint ? mbar_try_wait_hint(bar, parity, hint) : mbar_try_wait(bar, parity))) {
-    if (((++spins) & 1023u) == 0 && globaltimer() - t0 > WS_WATCHDOG_NS) {
-      ws_watchdog_record.block = blockIdx.x | (static_cast<unsigned long long>(blockIdx.y) << 32);
-      ws_watchdog_record.thread = threadIdx.x;
-      ws_watchdog_record.bar_smem = bar;
-      ws_watchdog_record.parity = parity;
-      ws_watchdog_record.tag = tag;
-      __threadfence_system();
-      asm volatile("trap;");
-    }
+    if (((++spins) & 1023u) == 0 && globaltimer() - t0 > WS_WATCHDOG_NS) ws_watchdog_fire(bar, parity, tag);
   }
 }
 

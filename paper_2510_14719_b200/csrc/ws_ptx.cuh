@@ -36,6 +36,8 @@ struct WatchdogRecord {
   unsigned int bar_smem;
   unsigned int parity;
   unsigned int tag;
+  unsigned int fired;  // set last (host-mapped copy: the record survives the trap)
+  unsigned int pad;
 };
 
 __device__ __forceinline__ uint64_t globaltimer() {

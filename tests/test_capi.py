@@ -18,7 +18,7 @@ def _declared_functions():
 
 def test_header_declares_the_path():
     assert _declared_functions() == ["ws_attn_fwd", "ws_attn_fwd_traced", "ws_debug_gemm_trace", "ws_gemm_tn", "ws_last_error",
-                                    "ws_launch_count", "ws_run_kernel", "ws_version"]
+                                    "ws_launch_count", "ws_run_kernel", "ws_version", "ws_watchdog"]
 
 
 def test_library_exports_every_declared_symbol(ws):
@@ -138,3 +138,33 @@ def test_product_package_never_imports_the_oracle():
                 src = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in src and "from oracle" not in src, f
                 assert "liboracle" not in src and "libwsref" not in src, f
+
+
+def test_trace_json_schema_from_a_synthetic_gemm_trace():
+    """trace.gemm_trace_json turns stamps into the reference's trace JSON (intervals / blocks /
+    summary with utilization = busy / cycles, ref trace.hpp:15-22,59-83) — host logic, no GPU."""
+    import numpy as np
+    from paper_2510_14719_b200 import trace
+    t = np.zeros((2, 32, 16), dtype=np.int64)
+    for ti in range(3):
+        b = 1000 + ti * 10000
+        t[0, ti, 12], t[0, ti, 13] = b, b + 8000              # producer
+        t[0, ti, 0], t[0, ti, 1], t[0, ti, 5], t[0, ti, 4] = b + 50, b + 100, b + 300, b + 9000  # MMA
+        t[0, ti, 6], t[0, ti, 7], t[0, ti, 8] = b + 9500, b + 9900, b + 11000  # epilogue half 0
+        t[0, ti, 9], t[0, ti, 10], t[0, ti, 11] = b + 9700, b + 10000, b + 11500
+    j = trace.gemm_trace_json(t)
+    assert set(j) == {"intervals", "blocks", "summary"}
+    s = j["summary"]
+    assert s["verdict"] == "completed" and s["cycles"] == max(iv["end"] for iv in j["intervals"] + j["blocks"])
+    assert set(s["utilization"]) == {"tma0", "tensor_core", "cuda_wg2"}
+    assert all(0.0 < u <= 1.0 for k, u in s["utilization"].items() if k != "cuda_wg2")
+    assert all(iv["start"] >= 0 and iv["end"] >= iv["start"] for iv in j["intervals"])
+    assert {b["reason"] for b in j["blocks"]} == {"wait tmem_empty (accumulator)", "wait full (first K block)"}
+    tc = [iv for iv in j["intervals"] if iv["unit"] == "tensor_core"]
+    assert len(tc) == 3 and tc[0]["end"] - tc[0]["start"] == 8700
+
+
+def test_watchdog_reports_nothing_without_a_timeout(ws):
+    """ws_watchdog is callable without a GPU and reports no Deadlock when no wait has timed out."""
+    from paper_2510_14719_b200 import trace
+    assert trace.watchdog() is None
