@@ -83,6 +83,10 @@ typedef struct ws_gemm_desc {
   int32_t group_m;             /* raster: tiles grouped by this many M-blocks; 0 = auto */
   int32_t act;                 /* epilogue activation: 0 none, 1 relu (gemm_act.k, ref
                                   proj/kernels/gemm_act.k:10-16) */
+  int32_t batch;               /* independent products stacked along rows, one launch (gemm_batched.k,
+                                  ref proj/kernels/gemm_batched.k:1-22): A [batch*M, K], B
+                                  [batch*N, K], C [batch*M, N]; product i uses rows i*M / i*N.
+                                  0 or 1 = a single product */
 } ws_gemm_desc;
 
 /* FlashAttention forward. q,k,v,o: [B, H, S, Dh] contiguous; lse: [B, H, S] fp32 (natural log,

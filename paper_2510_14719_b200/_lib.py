@@ -33,7 +33,7 @@ class GemmDesc(ctypes.Structure):
         ("D", ctypes.c_int32), ("P", ctypes.c_int32),
         ("persistent", ctypes.c_int32), ("cta_pair", ctypes.c_int32),
         ("bn", ctypes.c_int32), ("group_m", ctypes.c_int32),
-        ("act", ctypes.c_int32),
+        ("act", ctypes.c_int32), ("batch", ctypes.c_int32),
     ]
 
 

@@ -203,6 +203,8 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   p.N = (int)d.N;
   p.K = (int)d.K;
   p.num_m_blocks = (int)(d.M / GEMM_BM);
+  const int64_t nbat = d.batch > 1 ? d.batch : 1;
+  p.batch = (int)nbat;
   p.num_n_blocks = (int)(d.N / BN);
   p.num_k_blocks = (int)(d.K / kbox);
   const GemmSmemLayout L1 = gemm_smem_layout(BN / CG, 1);
@@ -233,17 +235,19 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
 
   CUtensorMap ta, tb, tc;
   ws_status s;
-  if ((s = make_tmap(&ta, d.A, in_dt, d.M, d.K, d.lda, GEMM_BM, kbox, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
+  if ((s = make_tmap(&ta, d.A, in_dt, nbat * d.M, d.K, d.lda, GEMM_BM, kbox, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) !=
+      WS_OK)
     return s;
-  if ((s = make_tmap(&tb, d.B, in_dt, d.N, d.K, d.ldb, (BN > 256 ? 256 : BN) / CG, kbox,
+  if ((s = make_tmap(&tb, d.B, in_dt, nbat * d.N, d.K, d.ldb, (BN > 256 ? 256 : BN) / CG, kbox,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) != WS_OK)
     return s;
   const int cw = 128 / elem_bytes(out_dt);
-  if ((s = make_tmap(&tc, d.C, out_dt, d.M, d.N, d.ldc, 32, cw, CU_TENSOR_MAP_L2_PROMOTION_NONE)) != WS_OK) return s;
+  if ((s = make_tmap(&tc, d.C, out_dt, nbat * d.M, d.N, d.ldc, 32, cw, CU_TENSOR_MAP_L2_PROMOTION_NONE)) != WS_OK)
+    return s;
 
   auto kern = ws_gemm_tn_kernel<IN, OUT, BN, CG>;
   WS_CUDA_CHECK(allow_smem(reinterpret_cast<const void*>(kern), (int)L.total));
-  const int tiles = (p.num_m_blocks / CG) * p.num_n_blocks;
+  const int tiles = (p.num_m_blocks / CG) * p.num_n_blocks * p.batch;
   const int units = num_sms() / CG;  // persistent: one CTA (pair) per SM (pair)
   int grid = CG * (d.persistent ? (tiles < units ? tiles : units) : tiles);
   cudaLaunchConfig_t cfg = {};
@@ -604,8 +608,9 @@ ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
   // ... and only when the grid still fills the GPU: small problems take the smaller tile with
   // more work units (1024^3: 128 x 128 single-CTA tiles, 64 CTAs)
   const int64_t units = num_sms();
-  const bool fill512 = (d.M / 256) * (d.N / 512) >= units / 2;
-  const bool fill256 = (d.M / 128) * (d.N / 256) >= units;
+  const int64_t nbat = d.batch > 1 ? d.batch : 1;
+  const bool fill512 = nbat * (d.M / 256) * (d.N / 512) >= units / 2;
+  const bool fill256 = nbat * (d.M / 128) * (d.N / 256) >= units;
   int bn = d.bn > 0 ? d.bn
            : (d.cta_pair && kblocks >= 16 && d.N % 512 == 0 && fill512) ? 512
            : (!d.cta_pair && !fill256 && d.N % 128 == 0)                 ? 128
@@ -618,6 +623,9 @@ ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
   if (d.K % (128 / eb))
     return fail(WS_INDIVISIBLE_TILE, "K=" + std::to_string(d.K) + " is not a multiple of " + std::to_string(128 / eb));
   if (d.lda < d.K || d.ldb < d.K || d.ldc < d.N) return fail(WS_TYPE, "leading dimension smaller than the row");
+  if (d.batch < 0) return fail(WS_TYPE, "batch must be >= 0 (0 or 1 = one product)");
+  if (nbat * d.M >= (int64_t)1 << 31 || nbat * d.N >= (int64_t)1 << 31)
+    return fail(WS_TYPE, "batch*M and batch*N must fit in int32");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
   return bn == 512 ? dispatch_in<512>(d, st) : bn == 256 ? dispatch_in<256>(d, st) : dispatch_in<128>(d, st);
 }

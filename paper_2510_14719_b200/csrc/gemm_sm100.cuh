@@ -45,6 +45,7 @@ struct GemmParams {
   unsigned long long* trace;
   int trace_global;  // stamps from %globaltimer (ns, comparable across SMs) instead of %clock64
   int debug_deadlock;  // WS_DEBUG_DEADLOCK: CTA 0 skips its first put (watchdog demonstration)
+  int batch;           // independent products stacked along rows (gemm_batched.k); >= 1
 };
 
 struct GemmSmemLayout {
@@ -75,6 +76,17 @@ __device__ __forceinline__ void gemm_tile_coords(int t, const GemmParams& p, int
   int r = t - g * per_group;
   mb = first_m + r % gsize;
   nb = r / gsize;
+}
+
+// Batched (ref proj/kernels/gemm_batched.k:1-22): products stacked along rows, a [batch*M, K],
+// b [batch*N, K], c [batch*M, N]; tile t = bi * tiles_per_batch + t' (the .k's pid = batch*T + tile).
+// Returns the row offsets of batch bi in A/C (bi*M) and B (bi*N).
+__device__ __forceinline__ void gemm_batch_coords(int t, const GemmParams& p, int tiles_per_batch, int num_m,
+                                                  int& mb, int& nb, int& a_off, int& b_off) {
+  const int bi = t / tiles_per_batch;
+  gemm_tile_coords(t - bi * tiles_per_batch, p, num_m, mb, nb);
+  a_off = bi * p.M;
+  b_off = bi * p.N;
 }
 
 // CG = 1: one CTA computes a 128 x BN tile.
@@ -114,7 +126,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
-  const int num_tiles = (p.num_m_blocks / CG) * p.num_n_blocks;  // pair tiles when CG == 2
+  const int tiles_per_batch = (p.num_m_blocks / CG) * p.num_n_blocks;  // pair tiles when CG == 2
+  const int num_tiles = tiles_per_batch * p.batch;
   const uint32_t D = static_cast<uint32_t>(p.stages);
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
   const bool leader = rank == 0;
@@ -155,10 +168,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       ArefCursor c;
       int ti = 0;
       for (int t = tile0; t < num_tiles; t += tile_stride, ++ti) {
-        int mb, nb;
-        gemm_tile_coords(t, p, p.num_m_blocks / CG, mb, nb);
-        const int arow = mb * GEMM_BM * CG + static_cast<int>(rank) * GEMM_BM;
-        const int brow = nb * BN + static_cast<int>(rank) * B_BOX;  // + h * MMA_N for half h
+        int mb, nb, a_off, b_off;
+        gemm_batch_coords(t, p, tiles_per_batch, p.num_m_blocks / CG, mb, nb, a_off, b_off);
+        const int arow = a_off + mb * GEMM_BM * CG + static_cast<int>(rank) * GEMM_BM;
+        const int brow = b_off + nb * BN + static_cast<int>(rank) * B_BOX;  // + h * MMA_N for half h
         for (int kb = 0; kb < p.num_k_blocks; ++kb) {
           ring->put_acquire(c, 1);
           if (kb == 0) GT(ti, 12);
@@ -336,9 +349,9 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     const bool tw = lane == 0 && q == 0;  // warps 4 (column half 0) and 8 (half 1) stamp events
     int ti = 0;
     for (int t = tile0; t < num_tiles; t += tile_stride, ++ti) {
-      int mb, nb;
-      gemm_tile_coords(t, p, p.num_m_blocks / CG, mb, nb);
-      const int crow = mb * GEMM_BM * CG + static_cast<int>(rank) * GEMM_BM;
+      int mb, nb, c_off, b_off_unused;
+      gemm_batch_coords(t, p, tiles_per_batch, p.num_m_blocks / CG, mb, nb, c_off, b_off_unused);
+      const int crow = c_off + mb * GEMM_BM * CG + static_cast<int>(rank) * GEMM_BM;
       auto cvt2 = [&](uint32_t a, uint32_t b) -> uint32_t {
         float f0 = __uint_as_float(a), f1 = __uint_as_float(b);
         if (!plain) {

@@ -47,7 +47,8 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
             out_dtype: Optional[torch.dtype] = None, scale_a: float = 1.0, scale_b: float = 1.0,
             D: int = 0, P: int = 0, persistent: bool = True, cta_pair: Optional[bool] = None, bn: int = 0,
             group_m: int = 0, stream: Optional[torch.cuda.Stream] = None) -> torch.Tensor:
-    """c[M,N] = scale_a*scale_b * a[M,K] . b[N,K]^T with fp32 accumulation on the tensor cores.
+    """c[M,N] = scale_a*scale_b * a[M,K] . b[N,K]^T with fp32 accumulation on the tensor cores
+    (or, for 3-D a [batch,M,K] and b [batch,N,K], every product of the batch in one launch).
 
     a, b: row-major (last dim contiguous) CUDA tensors of dtype f16/bf16/float8_e4m3fn.
     out: optional [M,N] tensor (may be a column slice of a wider matrix; its row stride is ldc).
@@ -59,23 +60,37 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
         raise _lib.WsError(2, "operands must be CUDA tensors (no CPU path)")
     if a.dtype != b.dtype or a.dtype not in (torch.float16, torch.bfloat16, torch.float8_e4m3fn):
         raise _lib.WsError(2, f"unsupported operand dtypes {a.dtype}, {b.dtype}")
-    M, K = a.shape
-    N, K2 = b.shape
+    # [batch, M, K] x [batch, N, K] -> [batch, M, N]: one launch over every product (the .k's
+    # gemm_batched, ref proj/kernels/gemm_batched.k:1-22); each operand's batches must be stacked
+    # rows (stride(0) = rows * stride(1)), which the 2-D tensor maps then walk as one matrix
+    batched = a.dim() == 3
+    if batched != (b.dim() == 3) or a.dim() not in (2, 3):
+        raise _lib.WsError(2, "a and b must both be 2-D, or both 3-D [batch, rows, K]")
+    nbat = a.shape[0] if batched else 1
+    if batched and b.shape[0] != nbat:
+        raise _lib.WsError(2, f"batch sizes disagree: {nbat} vs {b.shape[0]}")
+    M, K = a.shape[-2:]
+    N, K2 = b.shape[-2:]
     if K != K2:
         raise _lib.WsError(2, f"inner dimensions disagree: {K} vs {K2}")
-    if a.stride(1) != 1 or b.stride(1) != 1:
+    if a.stride(-1) != 1 or b.stride(-1) != 1:
         raise _lib.WsError(2, "operands must be K-contiguous (row-major)")
+    if batched and (a.stride(0) != M * a.stride(1) or b.stride(0) != N * b.stride(1)):
+        raise _lib.WsError(2, "batched operands must stack their batches along rows")
     if cta_pair is None:
         # pairs only when the 256 x 256 pair tiles still give every SM pair a tile
-        cta_pair = M % 256 == 0 and K >= 256 and (M // 256) * (N // 256) >= _sm_count(a.device) // 2
+        cta_pair = M % 256 == 0 and K >= 256 and nbat * (M // 256) * (N // 256) >= _sm_count(a.device) // 2
+    shape = (nbat, M, N) if batched else (M, N)
     if out is None:
         od = out_dtype or (torch.bfloat16 if a.dtype == torch.float8_e4m3fn else a.dtype)
-        out = torch.empty((M, N), dtype=od, device=a.device)
-    if out.stride(1) != 1 or tuple(out.shape) != (M, N):
-        raise _lib.WsError(2, "out must be [M, N] with contiguous rows")
+        out = torch.empty(shape, dtype=od, device=a.device)
+    if out.stride(-1) != 1 or tuple(out.shape) != shape or (batched and out.stride(0) != M * out.stride(1)):
+        raise _lib.WsError(2, f"out must be {list(shape)} with contiguous rows" +
+                           (" and batches stacked along rows" if batched else ""))
+    lda, ldb, ldc = a.stride(-2), b.stride(-2), out.stride(-2)
     # descriptors are reused for repeated calls on the same buffers and knobs (host cost per call
     # matters for small GEMMs; scripts/host_overhead.py)
-    key = (a.data_ptr(), b.data_ptr(), out.data_ptr(), M, N, K, a.stride(0), b.stride(0), out.stride(0),
+    key = (a.data_ptr(), b.data_ptr(), out.data_ptr(), M, N, K, lda, ldb, ldc, nbat,
            a.dtype, out.dtype, scale_a, scale_b, D, P, persistent, cta_pair, bn, group_m)
     d = _DESC_CACHE.get(key)
     if d is None:
@@ -83,9 +98,10 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
         d.in_dtype = _DT[a.dtype]
         d.out_dtype = _DT[out.dtype]
         d.M, d.N, d.K = M, N, K
-        d.A, d.lda = a.data_ptr(), a.stride(0)
-        d.B, d.ldb = b.data_ptr(), b.stride(0)
-        d.C, d.ldc = out.data_ptr(), out.stride(0)
+        d.A, d.lda = a.data_ptr(), lda
+        d.B, d.ldb = b.data_ptr(), ldb
+        d.C, d.ldc = out.data_ptr(), ldc
+        d.batch = nbat
         d.scale_a, d.scale_b = scale_a, scale_b
         d.D, d.P = D, P
         d.persistent, d.cta_pair, d.bn, d.group_m = int(persistent), int(cta_pair), bn, group_m

@@ -217,3 +217,29 @@ def test_pair_512_many_tiles_per_pair_16bit(ws, dev):
     rows = np.array([0, 255, 256, 4095, 4096, 8191] + list(np.random.default_rng(7).integers(0, M, 10)))
     want = torch.from_numpy(_want(M, N, K, rows=rows)).to(dev).to(BF16)
     assert torch.equal(c[torch.from_numpy(rows).to(dev)], want)
+
+
+@pytest.mark.parametrize("kw", [dict(cta_pair=False, bn=256), dict(cta_pair=False, bn=128), dict(cta_pair=True, bn=256),
+                                dict(cta_pair=True, bn=512), {}])
+def test_batched_one_launch_bit_exact(ws, dev, kw):
+    """gemm_batched.k semantics (ref proj/kernels/gemm_batched.k:1-22): products stacked along rows,
+    one launch over batch x tiles; every product equals the oracle exactly (fp32 out)."""
+    nb, M, N, K = 3, 512, 1024, 320
+    a = torch.stack([ref_tensor(f"a{i}", (M, K), BF16, dev) for i in range(nb)])
+    b = torch.stack([ref_tensor(f"b{i}", (N, K), BF16, dev) for i in range(nb)])
+    n0 = ws.launch_count()
+    c = ws.gemm_tn(a, b, out_dtype=F32, **kw)
+    torch.cuda.synchronize()
+    assert ws.launch_count() == n0 + 1 and tuple(c.shape) == (nb, M, N)
+    for i in range(nb):
+        want = oracle.gemm(oracle.generate_real(f"a{i}", (M, K)), oracle.generate_real(f"b{i}", (N, K)))
+        assert np.array_equal(as_f64(c[i]), want), (i, kw)
+
+
+def test_batched_rejects_unstacked_operands(ws, dev):
+    a = torch.zeros(2, 256, 128, dtype=BF16, device=dev)
+    b = torch.zeros(2, 256, 128, dtype=BF16, device=dev)
+    with pytest.raises(ws.WsError):
+        ws.gemm_tn(a.transpose(0, 1).contiguous().transpose(0, 1), b)  # batches interleaved, not stacked
+    with pytest.raises(ws.WsError):
+        ws.gemm_tn(a, b[:1])
