@@ -243,3 +243,16 @@ def test_batched_rejects_unstacked_operands(ws, dev):
         ws.gemm_tn(a.transpose(0, 1).contiguous().transpose(0, 1), b)  # batches interleaved, not stacked
     with pytest.raises(ws.WsError):
         ws.gemm_tn(a, b[:1])
+
+
+def test_batched_fp8_scaled_bf16_out(ws, dev):
+    """FP8 e4m3 batched launch with per-tensor scales and 16-bit output (256 x 512 pair tiles):
+    each product equals the oracle rounded once to bf16 (power-of-two scales keep it exact)."""
+    nb, M, N, K = 2, 512, 1024, 2048
+    a = torch.stack([ref_tensor(f"a{i}", (M, K), E4M3, dev) for i in range(nb)])
+    b = torch.stack([ref_tensor(f"b{i}", (N, K), E4M3, dev) for i in range(nb)])
+    c = ws.gemm_tn(a, b, out_dtype=BF16, scale_a=0.5, scale_b=0.25, cta_pair=True, bn=512)
+    torch.cuda.synchronize()
+    for i in range(nb):
+        want = oracle.gemm(oracle.generate_real(f"a{i}", (M, K)), oracle.generate_real(f"b{i}", (N, K)), scale=0.125)
+        assert torch.equal(c[i], torch.from_numpy(want).to(dev).to(BF16)), i
