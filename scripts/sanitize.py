@@ -9,6 +9,11 @@ dev = torch.device("cuda")
 a = torch.randn(512, 1024, device=dev).bfloat16(); b = torch.randn(1024, 1024, device=dev).bfloat16()
 for kw in ({"cta_pair": False}, {"cta_pair": True, "bn": 256}, {"cta_pair": True, "bn": 512}):
     ws.gemm_tn(a, b, **kw)
+# several 256 x 512 tiles per CTA pair: the half-by-half accumulator hand-over and the
+# early-release epilogue across tiles; and a batched launch
+a2 = torch.randn(4096, 256, device=dev).bfloat16(); b2 = torch.randn(8192, 256, device=dev).bfloat16()
+ws.gemm_tn(a2, b2, cta_pair=True, bn=512)
+ws.gemm_tn(a2.view(2, 2048, 256), b2.view(2, 4096, 256), cta_pair=True, bn=512)
 a8, b8 = a.to(torch.float8_e4m3fn), b.to(torch.float8_e4m3fn)
 ws.gemm_tn(a8, b8, cta_pair=True)
 q = torch.randn(1, 2, 512, 128, device=dev).bfloat16(); k = torch.randn_like(q); v = torch.randn_like(q)
