@@ -88,6 +88,9 @@ def gemm_tn_host(jobs: Sequence[Tuple[torch.Tensor, torch.Tensor, torch.Tensor]]
         dc = p.buf(("c", slot), c.shape, c.dtype)
         M = a.shape[0]
         n = _row_chunks(M, c.numel() * c.element_size(), row_chunks)
+        if row_chunks is None and i == len(jobs) - 1:
+            # the last job's final chunk (its GEMM and copy-out) is the pipeline's exposed tail
+            n = _row_chunks(M, c.numel() * c.element_size(), 2 * n)  # 2x: 22.8 vs 23.2 ms (4x, 8x slower)
         rows = M // n
         # H2D(i) after every GEMM of job i-2 has read the slot
         if p.gemm_done[slot] is not None:
