@@ -93,7 +93,8 @@ typedef struct ws_gemm_desc {
  * lse = m + log(l)); may be NULL. Only bh in [bh_begin, bh_end) is computed (the multi-GPU
  * batch*heads shard); bh_end <= 0 means B*H. dtype in {BF16, F16, E4M3 (Dh 128; o is BF16;
  * P is quantized to e4m3 for the P.V product)}; Dh in {64, 128};
- * S % 128 == 0. softmax_scale <= 0 means 1/sqrt(Dh). */
+ * S % 128 == 0 (kv_block 64 and the P-in-TMEM developer kernel: S % 256 == 0).
+ * softmax_scale <= 0 means 1/sqrt(Dh). */
 typedef struct ws_attn_desc {
   int32_t dtype;
   int32_t B, H, S, Dh;

@@ -327,6 +327,9 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     item_coords(item, pair, bh);
     const int n_t = nblk(pair, t);
     const int q_row0 = bh * p.S + pair * 2 * A128_BM;
+    // S % 256 == 128: the last pair's second tile lies past the sequence — computed on whatever the
+    // loads return (the next (b,h)'s rows, or TMA zero fill) and never stored
+    const bool tile_valid = (2 * pair + t) * A128_BM < p.S;
     const int j_diag = p.causal ? n_t - 1 : -1;
     float m_used = -INFINITY;  // running max (log2 units) the current P/O are relative to
     float l = 0.f;
@@ -511,13 +514,13 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       }
       fence_proxy_async_smem();
       named_bar_sync(1 + t, 128);
-      if (warp == 4u * t && lane == 0) {
+      if (warp == 4u * t && lane == 0 && tile_valid) {
         tma_store_2d(&tm_o, reinterpret_cast<const void*>(sp + t * PTILE + (c % PPANELS) * PANEL), c * 64,
                      q_row0 + t * A128_BM);
         tma_store_commit();
       }
     }
-    if (p.lse) p.lse[grow] = m_used * 0.69314718055994531f + __logf(l);
+    if (p.lse && tile_valid) p.lse[grow] = m_used * 0.69314718055994531f + __logf(l);
     if (tr) WS_TRACE(1 + t, g - 1, 7);
     }  // items
     if (warp == 4u * t && lane == 0) tma_store_wait<0>();  // O stores complete before the CTA retires

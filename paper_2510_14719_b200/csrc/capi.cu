@@ -317,6 +317,8 @@ ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stre
   p.S = d.S;
   p.Dh = DH;
   p.BH_begin = bh0;
+  if (d.S % (2 * ATTN_BM))
+    return fail(WS_INDIVISIBLE_TILE, "the 64-key kernel needs S % 256 == 0 (S=" + std::to_string(d.S) + ")");
   p.num_pairs = d.S / (2 * ATTN_BM);
   p.causal = d.causal;
   const float sm = d.softmax_scale > 0.f ? d.softmax_scale : 1.0f / std::sqrt((float)DH);
@@ -355,12 +357,14 @@ ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stre
 template <int DH, bool BF16, bool PSMEM>
 ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stream, unsigned long long* trace) {
   using namespace ws;
+  if (!PSMEM && d.S % (2 * A128_BM))
+    return fail(WS_INDIVISIBLE_TILE, "the P-in-TMEM kernel needs S % 256 == 0 (S=" + std::to_string(d.S) + ")");
   const int dt = d.dtype;
   const int64_t rows = (int64_t)d.B * d.H * d.S;
   Attn128Params p;
   p.S = d.S;
   p.BH_begin = bh0;
-  p.num_pairs = d.S / (2 * A128_BM);
+  p.num_pairs = (d.S + 2 * A128_BM - 1) / (2 * A128_BM);  // S % 256 == 128: last pair half valid
   p.num_bh = bh1 - bh0;
   static const int stagger_env = [] {  // WS_ATTN_STAGGER (developer knob)
     const char* e = getenv("WS_ATTN_STAGGER");
@@ -445,7 +449,7 @@ ws_status launch_attn_fp8(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t 
   Attn128Params p;
   p.S = d.S;
   p.BH_begin = bh0;
-  p.num_pairs = d.S / (2 * A128_BM);
+  p.num_pairs = (d.S + 2 * A128_BM - 1) / (2 * A128_BM);  // S % 256 == 128: last pair half valid
   p.num_bh = bh1 - bh0;
   p.stagger = 1;
   p.causal = d.causal;
@@ -515,7 +519,7 @@ ws_status attn_entry(const ws_attn_desc& d, cudaStream_t st, unsigned long long*
     return fail(WS_TYPE, "attention dtype must be BF16, F16 or E4M3");
   if (d.B <= 0 || d.H <= 0 || d.S <= 0) return fail(WS_TYPE, "B, H, S must be positive");
   if (d.Dh != 64 && d.Dh != 128) return fail(WS_UNSUPPORTED_KERNEL, "head dim must be 64 or 128");
-  if (d.S % 256) return fail(WS_INDIVISIBLE_TILE, "S=" + std::to_string(d.S) + " is not a multiple of 256");
+  if (d.S % 128) return fail(WS_INDIVISIBLE_TILE, "S=" + std::to_string(d.S) + " is not a multiple of 128");
   if (!d.Q || !d.K || !d.V || !d.O) return fail(WS_TYPE, "null operand pointer");
   if (d.D == 1) return fail(WS_PIPELINE_INFEASIBLE, "the K/V aref needs D >= 2 (ref pipeline.hpp:309-315)");
   if (d.D < 0) return fail(WS_PIPELINE_INFEASIBLE, "D must be >= 2 (0 = auto)");

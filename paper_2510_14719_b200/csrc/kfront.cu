@@ -835,8 +835,8 @@ bool try_flash(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo
     if (e2.get(lq->args[0]) != pid * BR || e2.get(lk->args[0]) != (pid / nqb) * S || e2.get(lv->args[0]) != (pid / nqb) * S)
       kfail(WS_UNSUPPORTED_KERNEL, "flash kernel pid geometry differs from the batched (b,h)-major layout");
   }
-  if ((D != 64 && D != 128) || S % 256 != 0)
-    kfail(WS_UNSUPPORTED_KERNEL, "flash on B200 needs head dim 64/128 and S % 256 == 0 (S=" + std::to_string(S) +
+  if ((D != 64 && D != 128) || S % 128 != 0)
+    kfail(WS_UNSUPPORTED_KERNEL, "flash on B200 needs head dim 64/128 and S % 128 == 0 (S=" + std::to_string(S) +
                                      ", D=" + std::to_string(D) + ")");
   const int64_t bh0 = lo / nqb, bh1 = (hi - 1) / nqb + 1;
   const size_t n = static_cast<size_t>(BH * S * D);

@@ -141,10 +141,43 @@ def test_c4_noncausal_sampled_blocks(ws, dev):
 
 
 def test_rejects_bad_shapes(ws, dev):
-    q = torch.zeros(1, 1, 384, 128, dtype=BF16, device=dev)
+    q = torch.zeros(1, 1, 320, 128, dtype=BF16, device=dev)
     with pytest.raises(ws.WsError) as e:
         ws.attn_fwd(q, q, q)
     assert e.value.code == "indivisible-tile"
+    q = torch.zeros(1, 1, 384, 128, dtype=BF16, device=dev)
+    with pytest.raises(ws.WsError) as e:
+        ws.attn_fwd(q, q, q, kv_block=64)  # the 64-key kernel pairs Q tiles: S % 256
+    assert e.value.code == "indivisible-tile"
+
+
+@pytest.mark.parametrize("S", [128, 384, 640])
+@pytest.mark.parametrize("Dh", [64, 128])
+@pytest.mark.parametrize("causal", [False, True])
+def test_odd_query_tile_count(ws, dev, S, Dh, causal):
+    """S % 256 == 128 (an odd number of 128-row query tiles, which the flash .k allows with BR = 128):
+    the last work item's second tile lies past the sequence and is never stored. Three (b,h)
+    slices, so a stray store would corrupt the next slice's rows, and the last slice ends at the
+    end of the tensors (its phantom tile reads TMA zero fill)."""
+    q, k, v = _inputs(1, 3, S, Dh, BF16, dev)
+    o = torch.full_like(q, float("nan"))
+    lse = torch.full((1, 3, S), float("nan"), device=dev)
+    ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse)
+    torch.cuda.synchronize()
+    assert not torch.isnan(o).any() and not torch.isnan(lse).any()
+    _check(q, k, v, o, lse, causal)
+
+
+@pytest.mark.parametrize("causal", [False, True])
+def test_odd_query_tile_count_fp8(ws, dev, causal):
+    B, H, S, Dh = 1, 3, 384, 128
+    q, k, v = (t.to(E4M3) for t in _inputs(B, H, S, Dh, BF16, dev))
+    o, lse = ws.attn_fwd(q, k, v, causal=causal)
+    torch.cuda.synchronize()
+    ro, rl = oracle.flash(as_f64(q), as_f64(k), as_f64(v), causal, block=128)
+    vmax = float(np.abs(as_f64(v)).max())
+    assert float(np.abs(as_f64(o) - ro).max()) <= 2.0 ** -4 * vmax
+    assert float(np.abs(as_f64(lse) - rl).max()) <= 1e-3
 
 
 E4M3 = torch.float8_e4m3fn

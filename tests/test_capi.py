@@ -104,7 +104,8 @@ def _attn_desc(ws, **kw):
 
 
 @pytest.mark.parametrize("kw,code", [
-    (dict(S=384), "indivisible-tile"),
+    (dict(S=320), "indivisible-tile"),
+    (dict(S=384, kv_block=64), "indivisible-tile"),  # the 64-key kernel pairs query tiles
     (dict(Dh=96), "unsupported-kernel"),
     (dict(D=1), "pipeline-infeasible"),             # coarse schedule needs D >= 2 (ref pipeline.hpp:309-315)
     (dict(D=9), "smem-overflow"),

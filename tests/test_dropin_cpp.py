@@ -55,3 +55,7 @@ def test_flash_through_the_reference_flow(ws, dev, tmp_path, causal):
     rc, log = _run(tmp_path, [K.flash_src(2, 256, 64, 128, causal)], "--pids", "4", "--flash")
     assert rc == 0, log
     assert "PASS" in log, log
+    # S = 384: three 128-row query blocks per slice (an odd count), 6 pids
+    rc, log = _run(tmp_path, [K.flash_src(2, 384, 64, 128, causal)], "--pids", "6", "--flash")
+    assert rc == 0, log
+    assert "PASS" in log, log

@@ -52,7 +52,7 @@ def test_attention_toy_is_not_flash(ws):
 
 def test_small_flash_is_refused_not_faked(ws):
     code, msg = _status(ws, K.flash_src(3, 64, 16, 16, causal=False))
-    assert code == "unsupported-kernel" and "S % 256" in msg
+    assert code == "unsupported-kernel" and "S % 128" in msg
 
 
 def test_buffer_shape_mismatch(ws):
