@@ -12,9 +12,12 @@
 //   warp 2      TMEM allocator
 //   warps 4..11 epilogue: tcgen05.ld -> scale/convert -> swizzled smem -> TMA store; two warps per
 //               TMEM lane quarter (warp w reads lanes 32*(w%4)..), each draining half the columns,
-//               with the next chunk's TMEM load in flight while the current one is converted
+//               with the next chunk's TMEM load in flight while the current one is converted.
+//               256 x 512 tiles with 16-bit output drain one N half at a time with all eight warps
+//               into registers and release it before storing (the early-release hand-over below)
 // Persistent scheduling (ref proj/include/warpspec/grid.hpp:93-123, run_grid :140-210): tile t
 // runs on CTA t mod gridDim.x; no per-tile barrier reset or quiesce — the aref phases carry over.
+// Batched launches (gemm_batched.k) extend the tile index over batch x tiles.
 #pragma once
 
 #include "ws_aref.cuh"
