@@ -388,6 +388,33 @@ def run_ours(args):
                                     "cublas_tflops": round(STEP_FLOPS / (med(ms_lib) * 1e-3) / 1e12, 1),
                                     "windows": "6 alternating windows of 3 sweeps each (no L2 flush), medians"}
 
+    # ---- strong-scaling shards ("expect wave-quantization loss; report it"): the
+    # work one GPU of G does when the global 8192 x 8192 sweep is N-column sharded G ways (B rows
+    # and a C column block of width 8192/G, ldc = 8192), timed here on this GPU ----
+    shards = {}
+    if world == 1 and not args.no_vs_cublas:
+        settle()
+        for G in (1, 2, 4, 8):
+            n_loc = N_ // G
+
+            def shard_sweep():
+                for K in K_SWEEP:
+                    a, b = ops[K]
+                    ws.gemm_tn(a, b[:n_loc], c[:, :n_loc])
+            shard_sweep()
+            reps = []
+            for _ in range(5):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                shard_sweep()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                reps.append(e0.elapsed_time(e1))
+            shards[str(G)] = {"ms_per_gpu_step": round(sorted(reps)[2], 4)}
+        t1 = shards["1"]["ms_per_gpu_step"]
+        for G, r in shards.items():
+            r["projected_strong_efficiency"] = round(t1 / (int(G) * r["ms_per_gpu_step"]), 3)
+
     # ---- attention path (C4 / C5), reported beside the headline ----
     settle()
     attn = bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier)
@@ -409,6 +436,7 @@ def run_ours(args):
         "tflops_per_k": per_k,
         "gemm_8192_cubed_tflops": per_k["8192"],
         "vs_cublas_same_box": lib,
+        "strong_scaling_shards": shards or None,
         "attention": attn,
         "other_configs": other_configs,
         "roofline": roofline,
