@@ -3,7 +3,7 @@
 Each variant runs in a subprocess (the knobs are read once per process); rounds alternate so
 clock/power drift hits every variant alike.
   python scripts/attn_ab.py 'WS_ATTN_PTMEM=1' 'WS_ATTN_PTMEM=0' ...
-AB_FP8=1 runs the hdim-128 cases with e4m3 inputs."""
+AB_FP8=1 runs the hdim-128 cases with e4m3 inputs; AB_SHORT=1 the C4 cases S = 1K / 2K / 4K."""
 import json, os, subprocess, sys
 
 CODE = r'''
@@ -13,6 +13,8 @@ import paper_2510_14719_b200 as ws
 res = {}
 fp8 = os.environ.get("AB_FP8") == "1"
 cases = [(1, 16384, 128, False), (1, 16384, 128, True), (16, 1024, 128, False), (1, 16384, 64, True), (1, 16384, 64, False)]
+if os.environ.get("AB_SHORT") == "1":  # the C4 short-sequence cases
+    cases = [(16, 1024, 128, False), (8, 2048, 128, False), (4, 4096, 128, False)]
 for (B, S, Dh, causal) in (cases[:3] if fp8 else cases):
     q = torch.randn(B, 16, S, Dh, device="cuda", dtype=torch.bfloat16); k = torch.randn_like(q); v = torch.randn_like(q)
     o = torch.empty_like(q); lse = torch.empty(B, 16, S, device="cuda")
