@@ -418,6 +418,9 @@ def run_ours(args):
     # ---- attention path (C4 / C5), reported beside the headline ----
     settle()
     attn = bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier)
+    if world == 1 and not args.no_vs_cublas:
+        settle()
+        attn["vs_trtllm_gen_fmha_same_box"] = bench_attention_vs_lib(ws, torch, dev, stream)
     settle()
     other_configs = bench_fp8_and_c1(ws, torch, dev, stream, args, world, max_over_ranks, barrier)
 
@@ -455,6 +458,50 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def bench_attention_vs_lib(ws, torch, dev, stream):
+    """Context, not part of `value`: our FA forward next to NVIDIA's trtllm-gen Blackwell FMHA
+    (flashinfer's prebuilt sm_100a cubins; library code, like cuBLAS for the GEMM) on the C4/C5
+    hdim-128 S=16K cases, alternating windows on this box (scripts/attn_vs_lib.py has more cases)."""
+    try:
+        import flashinfer  # noqa: F401
+        from scripts.attn_vs_lib import lib_arm
+    except Exception as e:  # noqa: BLE001
+        return {"unavailable": f"{type(e).__name__}: {str(e)[:120]}"}
+    res = {"_method": "alternating windows (0.3 s apart) of 10 launches, medians of 5; trtllm-gen ragged "
+                      "context FMHA, separate Q/K/V, LSE returned (as ours)"}
+    for name, causal in (("c4_noncausal_s16k_d128", False), ("c5_causal_s16k_d128", True)):
+        try:
+            q = torch.randn(1, 16, 16384, 128, device=dev, dtype=torch.bfloat16)
+            k, v = torch.randn_like(q), torch.randn_like(q)
+            o = torch.empty_like(q)
+            lse = torch.empty(1, 16, 16384, device=dev)
+            ours = lambda: ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse)
+            lib, _ = lib_arm(q, k, v, causal)
+            ours(); lib()
+            torch.cuda.synchronize()
+
+            def window(fn):
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                for _ in range(10):
+                    fn()
+                e1.record(stream)
+                torch.cuda.synchronize()
+                return e0.elapsed_time(e1) / 10
+            to, tl = [], []
+            for _ in range(5):
+                time.sleep(0.3)
+                to.append(window(ours))
+                time.sleep(0.3)
+                tl.append(window(lib))
+            fl = 4.0 * 16 * 16384 * 16384 * 128 / (2 if causal else 1)
+            mo, ml = sorted(to)[2], sorted(tl)[2]
+            res[name] = {"ours_tflops": round(fl / mo / 1e9, 1), "lib_tflops": round(fl / ml / 1e9, 1)}
+        except Exception as e:  # noqa: BLE001
+            res[name] = {"unavailable": f"{type(e).__name__}: {str(e)[:120]}"}
+    return res
 
 
 def bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier):
