@@ -256,3 +256,29 @@ def test_batched_fp8_scaled_bf16_out(ws, dev):
     for i in range(nb):
         want = oracle.gemm(oracle.generate_real(f"a{i}", (M, K)), oracle.generate_real(f"b{i}", (N, K)), scale=0.125)
         assert torch.equal(c[i], torch.from_numpy(want).to(dev).to(BF16)), i
+
+
+@pytest.mark.parametrize("M,N,K,out_dt,kw", [
+    (8192, 4096, 2048, F32, dict(cta_pair=True, bn=512)),     # 256 tiles over 74 pairs: a partial last wave
+    (8192, 4096, 2048, BF16, dict(cta_pair=True, bn=512)),    # the early-release path, 16-bit out
+    (4096, 4096, 1024, F32, dict(cta_pair=False, bn=256)),    # 512 single-CTA tiles over 148 CTAs
+    (8192, 4096, 4096, F16, dict(cta_pair=True, bn=512)),
+])
+def test_partial_last_wave_exact(ws, dev, M, N, K, out_dt, kw):
+    """The N-shard shapes of the strong-scaling projection (a partial last wave): exact against the
+    oracle (fp32 out; 16-bit out = the oracle rounded once). Every row through the row-sum
+    identity, sampled rows element by element, including the last M blocks in raster order."""
+    a = ref_tensor("a", (M, K), BF16, dev)
+    b = ref_tensor("b", (N, K), BF16, dev)
+    c = ws.gemm_tn(a, b, out_dtype=out_dt, **kw)
+    torch.cuda.synchronize()
+    if out_dt == F32:
+        assert torch.equal(c.double().sum(1), a.double() @ b.double().sum(0))
+    rows = np.array([0, 255, 256, M // 2, M - 257, M - 256, M - 129, M - 1]
+                    + list(np.random.default_rng(K).integers(0, M, 8)))
+    want = _want(M, N, K, rows=rows)
+    got = c[torch.from_numpy(rows).to(dev)]
+    if out_dt == F32:
+        assert np.array_equal(as_f64(got), want)
+    else:
+        assert torch.equal(got, torch.from_numpy(want).to(dev).to(out_dt))
