@@ -249,6 +249,12 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   WS_CUDA_CHECK(allow_smem(reinterpret_cast<const void*>(kern), (int)L.total));
   const int tiles = (p.num_m_blocks / CG) * p.num_n_blocks * p.batch;
   const int units = num_sms() / CG;  // persistent: one CTA (pair) per SM (pair)
+  // 256 x 512 tiles: a last wave at most half full runs its tiles as N-half units (one more short
+  // round instead of a long, mostly idle one)
+  p.half_from = tiles;
+  static const int half_env = getenv("WS_GEMM_HALF_TAIL") ? atoi(getenv("WS_GEMM_HALF_TAIL")) : 1;
+  if (BN == 512 && half_env && d.persistent && tiles > units && 2 * (tiles % units) <= units)
+    p.half_from = tiles - tiles % units;
   int grid = CG * (d.persistent ? (tiles < units ? tiles : units) : tiles);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
