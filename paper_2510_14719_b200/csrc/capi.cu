@@ -619,7 +619,16 @@ ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
   // more work units (1024^3: 128 x 128 single-CTA tiles, 64 CTAs)
   const int64_t units = num_sms();
   const int64_t nbat = d.batch > 1 ? d.batch : 1;
-  const bool fill512 = nbat * (d.M / 256) * (d.N / 512) >= units / 2;
+  // 256 x 512 vs 256 x 256 pairs by rounds of the persistent schedule: a K block takes ~1040 cycles
+  // in a 256x512 tile and ~712 (TMA-bound) in a 256x256 one; a last 256x512 round at most half full
+  // runs as N-half units (~712). One full round of 512-wide tiles beats two of 256-wide ones.
+  // (no device, e.g. validation-only calls on a CPU host: assume a B200's 74 SM pairs)
+  const int64_t pairs = units >= 2 ? units / 2 : 74, t512 = nbat * (d.M / 256) * (d.N / 512), t256 = 2 * t512;
+  const int64_t full512 = t512 / pairs, tail512 = t512 % pairs;
+  const double cost512 =
+      full512 * 1040.0 + (tail512 == 0 ? 0.0 : (full512 > 0 && 2 * tail512 <= pairs ? 712.0 : 1040.0));
+  const double cost256 = (double)((t256 + pairs - 1) / pairs) * 712.0;
+  const bool fill512 = cost512 <= cost256;
   const bool fill256 = nbat * (d.M / 128) * (d.N / 256) >= units;
   int bn = d.bn > 0 ? d.bn
            : (d.cta_pair && kblocks >= 16 && d.N % 512 == 0 && fill512) ? 512
