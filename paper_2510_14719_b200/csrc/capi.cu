@@ -249,12 +249,6 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   WS_CUDA_CHECK(allow_smem(reinterpret_cast<const void*>(kern), (int)L.total));
   const int tiles = (p.num_m_blocks / CG) * p.num_n_blocks * p.batch;
   const int units = num_sms() / CG;  // persistent: one CTA (pair) per SM (pair)
-  // 256 x 512 tiles: a last wave at most half full runs its tiles as N-half units (one more short
-  // round instead of a long, mostly idle one)
-  p.half_from = tiles;
-  static const int half_env = getenv("WS_GEMM_HALF_TAIL") ? atoi(getenv("WS_GEMM_HALF_TAIL")) : 1;
-  if (BN == 512 && half_env && d.persistent && tiles > units && 2 * (tiles % units) <= units)
-    p.half_from = tiles - tiles % units;
   int grid = CG * (d.persistent ? (tiles < units ? tiles : units) : tiles);
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -620,13 +614,12 @@ ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
   const int64_t units = num_sms();
   const int64_t nbat = d.batch > 1 ? d.batch : 1;
   // 256 x 512 vs 256 x 256 pairs by rounds of the persistent schedule: a K block takes ~1040 cycles
-  // in a 256x512 tile and ~712 (TMA-bound) in a 256x256 one; a last 256x512 round at most half full
-  // runs as N-half units (~712). One full round of 512-wide tiles beats two of 256-wide ones.
+  // in a 256x512 tile and ~712 (TMA-bound) in a 256x256 one. One full round of 512-wide tiles
+  // beats two of 256-wide ones.
   // (no device, e.g. validation-only calls on a CPU host: assume a B200's 74 SM pairs)
   const int64_t pairs = units >= 2 ? units / 2 : 74, t512 = nbat * (d.M / 256) * (d.N / 512), t256 = 2 * t512;
   const int64_t full512 = t512 / pairs, tail512 = t512 % pairs;
-  const double cost512 =
-      full512 * 1040.0 + (tail512 == 0 ? 0.0 : (full512 > 0 && 2 * tail512 <= pairs ? 712.0 : 1040.0));
+  const double cost512 = (double)(full512 + (tail512 ? 1 : 0)) * 1040.0;
   const double cost256 = (double)((t256 + pairs - 1) / pairs) * 712.0;
   const bool fill512 = cost512 <= cost256;
   const bool fill256 = nbat * (d.M / 128) * (d.N / 256) >= units;

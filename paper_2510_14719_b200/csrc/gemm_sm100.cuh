@@ -49,9 +49,6 @@ struct GemmParams {
   int trace_global;  // stamps from %globaltimer (ns, comparable across SMs) instead of %clock64
   int debug_deadlock;  // WS_DEBUG_DEADLOCK: CTA 0 skips its first put (watchdog demonstration)
   int batch;           // independent products stacked along rows (gemm_batched.k); >= 1
-  // 256 x 512 tiles only: tiles [half_from, tiles) (a short last wave) run as two N-half units
-  // each (256 x 256 of output, TMA-bound but twice as many units); half_from = tiles: off
-  int half_from;
 };
 
 struct GemmSmemLayout {
@@ -138,19 +135,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   const uint32_t rank = CG == 2 ? cluster_ctarank() : 0u;
   const bool leader = rank == 0;
   const int tile0 = static_cast<int>(blockIdx.x) / CG, tile_stride = static_cast<int>(gridDim.x) / CG;
-  // work units: whole tiles, then (NH == 2) the tail tiles as N-half units; hsel = the half a unit
-  // computes, -1 = both
-  const int half_from = NH == 2 ? p.half_from : num_tiles;
-  const int num_units = half_from + 2 * (num_tiles - half_from);
-  auto unit_of = [&](int u, int& t, int& hsel) {
-    if (u < half_from) {
-      t = u;
-      hsel = -1;
-    } else {
-      t = half_from + ((u - half_from) >> 1);
-      hsel = (u - half_from) & 1;
-    }
-  };
   unsigned long long* const trace = blockIdx.x < 2 ? p.trace : nullptr;
 #define GT(ti, ev)                                                                        \
   do {                                                                                    \
@@ -186,10 +170,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     if (lane == 0) {
       ArefCursor c;
       int ti = 0;
-      for (int u = tile0; u < num_units; u += tile_stride, ++ti) {
-        int t, hsel;
-        unit_of(u, t, hsel);
-        const uint32_t stage_tx = hsel < 0 ? L.stage_bytes : L.a_bytes + B_BOX * GEMM_ROW_BYTES;
+      for (int t = tile0; t < num_tiles; t += tile_stride, ++ti) {
         int mb, nb, a_off, b_off;
         gemm_batch_coords(t, p, tiles_per_batch, p.num_m_blocks / CG, mb, nb, a_off, b_off);
         const int arow = a_off + mb * GEMM_BM * CG + static_cast<int>(rank) * GEMM_BM;
@@ -206,20 +187,18 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           // coordinates are in elements of the tensor map's innermost dim (K) then rows
           const int kcoord = kb * (IN == IN_E4M3 ? 128 : 64);
           if constexpr (CG == 1) {
-            ring->put_expect(c, stage_tx);
+            ring->put_expect(c, L.stage_bytes);
             tma_load_2d(sa, &tm_a, &ring->full[c.slot], kcoord, arow);
 #pragma unroll
             for (int h = 0; h < NH; ++h)
-              if (hsel < 0 || h == hsel)
-                tma_load_2d(sb + h * B_BOX * GEMM_ROW_BYTES, &tm_b, &ring->full[c.slot], kcoord, brow + h * MMA_N);
+              tma_load_2d(sb + h * B_BOX * GEMM_ROW_BYTES, &tm_b, &ring->full[c.slot], kcoord, brow + h * MMA_N);
           } else {
             // the leader's full barrier collects both CTAs' bytes (one expect_tx for the pair)
-            if (leader) ring->put_expect(c, 2 * stage_tx);
+            if (leader) ring->put_expect(c, 2 * L.stage_bytes);
             tma_load_2d_cg2(sa, &tm_a, &ring->full[c.slot], kcoord, arow);
 #pragma unroll
             for (int h = 0; h < NH; ++h)
-              if (hsel < 0 || h == hsel)
-                tma_load_2d_cg2(sb + h * B_BOX * GEMM_ROW_BYTES, &tm_b, &ring->full[c.slot], kcoord, brow + h * MMA_N);
+              tma_load_2d_cg2(sb + h * B_BOX * GEMM_ROW_BYTES, &tm_b, &ring->full[c.slot], kcoord, brow + h * MMA_N);
           }
           c.advance(D);
         }
@@ -234,9 +213,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
       uint32_t acc_stage = 0, acc_phase = 0;
       const uint32_t P = static_cast<uint32_t>(p.mma_depth);
       // MMAs of one N half of one staged K block
-      int hsel = -1;  // the current unit's only N half (-1: both)
       auto issue_half = [&](uint32_t slot, int h, int kb) {
-        if (hsel >= 0 && h != hsel) return;  // half units: the other half's MMAs are skipped
         const uint32_t sa = smem_u32(smem + slot * L.stage_bytes);
         const uint32_t sb = sa + L.a_bytes + h * B_BOX * GEMM_ROW_BYTES;
         const uint32_t d = tmem_base + acc_stage * BN + h * MMA_N;
@@ -271,9 +248,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         uint32_t pend_slot[GEMM_MAX_STAGES];
         int pend_kb[GEMM_MAX_STAGES];
         int ti = 0;
-        for (int u = tile0; u < num_units; u += tile_stride, ++ti) {
-          int t_unused;
-          unit_of(u, t_unused, hsel);
+        for (int t = tile0; t < num_tiles; t += tile_stride, ++ti) {
           const uint32_t par = acc_phase ^ 1u;
           GT(ti, 0);
           mbar_wait(&tmem_empty[0], par, 3);
@@ -329,9 +304,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
       } else {
         int ti = 0;
-        for (int u = tile0; u < num_units; u += tile_stride, ++ti) {
-          int t_unused;
-          unit_of(u, t_unused, hsel);
+        for (int t = tile0; t < num_tiles; t += tile_stride, ++ti) {
           GT(ti, 0);
           mbar_wait(&tmem_empty[acc_stage], acc_phase ^ 1u, 3);
           if (NH == 2) mbar_wait(&tmem_empty[1], acc_phase ^ 1u, 3);
@@ -378,9 +351,7 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     };
     const bool tw = lane == 0 && q == 0;  // warps 4 (column half 0) and 8 (half 1) stamp events
     int ti = 0;
-    for (int u = tile0; u < num_units; u += tile_stride, ++ti) {
-      int t, hsel;
-      unit_of(u, t, hsel);
+    for (int t = tile0; t < num_tiles; t += tile_stride, ++ti) {
       int mb, nb, c_off, b_off_unused;
       gemm_batch_coords(t, p, tiles_per_batch, p.num_m_blocks / CG, mb, nb, c_off, b_off_unused);
       const int crow = c_off + mb * GEMM_BM * CG + static_cast<int>(rank) * GEMM_BM;
@@ -432,10 +403,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           mbar_wait(&tmem_full[h], acc_phase, 5);
           tc_fence_after();
           if (tw && hc == 0) GT(ti, 6 + 3 * h);
-          if (hsel >= 0 && h != hsel) {  // a half unit: this half holds nothing; keep the phases
-            release_acc(h, 7 + 3 * h);
-            continue;
-          }
           const uint32_t t_row = tmem_base + ((q * 32u) << 16) + h * MMA_N + hc * HC;
           uint32_t pk[HC / 2];
           uint32_t va[16], vb[16];
@@ -464,7 +431,6 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         mbar_wait(&tmem_full[bar], acc_phase, 5);
         tc_fence_after();
         if (tw) GT(ti, 6 + 3 * hc);
-        const bool skip = NH == 2 && hsel >= 0 && hc != hsel;  // a half unit's other half: nothing to drain
         const uint32_t t_row = tmem_base + ((q * 32u) << 16) + acc_stage * BN + hc * (BN / 2);
         // one chunk: CW columns = 128 bytes of output per row
         auto chunk = [&](uint32_t(&cur)[CW], uint32_t(&nxt)[CW], int ch) {
@@ -485,16 +451,12 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           }
           stage_store(w, nb * BN + hc * (BN / 2) + ch * CW);
         };
-        if (skip) {
-          release_acc(bar, 7 + 3 * hc);
-        } else {
-          uint32_t va[CW], vb[CW];
-          tmem_load(t_row, va);
+        uint32_t va[CW], vb[CW];
+        tmem_load(t_row, va);
 #pragma unroll 1
-          for (int ch = 0; ch < NCHW; ch += 2) {
-            chunk(va, vb, ch);
-            if (ch + 1 < NCHW) chunk(vb, va, ch + 1);
-          }
+        for (int ch = 0; ch < NCHW; ch += 2) {
+          chunk(va, vb, ch);
+          if (ch + 1 < NCHW) chunk(vb, va, ch + 1);
         }
         if (tw) GT(ti, 8 + 3 * hc);
       }
