@@ -169,3 +169,15 @@ def test_watchdog_reports_nothing_without_a_timeout(ws):
     """ws_watchdog is callable without a GPU and reports no Deadlock when no wait has timed out."""
     from paper_2510_14719_b200 import trace
     assert trace.watchdog() is None
+
+
+def test_host_pipeline_row_chunk_policy():
+    """gemm_tn_host's row chunking (host logic): ~32 MB of C per chunk, whole 256-row pair blocks,
+    an explicit count reduced until it divides M into such blocks."""
+    from paper_2510_14719_b200.hostpipe import _row_chunks
+    assert _row_chunks(8192, 8192 * 8192 * 2, None) == 4        # 128 MB of bf16 C -> 4 chunks
+    assert _row_chunks(8192, 8192 * 8192 * 2, 8) == 8
+    assert _row_chunks(256, 256 * 512 * 4, None) == 1
+    assert _row_chunks(768, 768 * 768 * 4, 4) == 3             # 4 does not divide 768 into 256-row blocks
+    assert _row_chunks(1024, 1024 * 512 * 4, 2) == 2
+    assert _row_chunks(640, 640 * 768 * 4, 4) == 1             # 640 rows: no whole 256-row split
