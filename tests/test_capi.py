@@ -181,3 +181,25 @@ def test_host_pipeline_row_chunk_policy():
     assert _row_chunks(768, 768 * 768 * 4, 4) == 3             # 4 does not divide 768 into 256-row blocks
     assert _row_chunks(1024, 1024 * 512 * 4, 2) == 2
     assert _row_chunks(640, 640 * 768 * 4, 4) == 1             # 640 rows: no whole 256-row split
+
+
+def test_trace_json_schema_from_a_synthetic_attention_trace():
+    """trace.attn_trace_json (host logic): MMA issue spans, softmax spans per warpgroup, epilogue
+    intervals and the waits on S / P become the reference's intervals / blocks / summary."""
+    import numpy as np
+    from paper_2510_14719_b200 import trace
+    t = np.zeros((3, 256, 8), dtype=np.int64)
+    for j in range(4):
+        b = 10_000 + 3000 * j
+        t[0, j, :6] = [b, b + 100, b + 200, b + 900, b + 1500, b + 1700]      # MMA issuer
+        for tt in (0, 1):
+            o = 300 * tt
+            t[1 + tt, j, :6] = [b + o, b + o + 150, b + o + 400, b + o + 600, b + o + 1300, b + o + 1450]
+    t[1, 3, 6], t[1, 3, 7] = 22_000, 23_000                                  # tile 0 epilogue
+    j = trace.attn_trace_json(t)
+    s = j["summary"]
+    assert s["verdict"] == "completed" and set(s["utilization"]) == {"tensor_core", "cuda_wg1", "cuda_wg2"}
+    assert len([iv for iv in j["intervals"] if iv["unit"] == "tensor_core"]) == 4
+    assert any(iv["label"] == "epilogue3" for iv in j["intervals"])
+    assert {b["reason"] for b in j["blocks"]} >= {"wait p_full[0]", "wait p_full[1]", "wait s_full[0]", "wait s_full[1]"}
+    assert all(0 <= iv["start"] <= iv["end"] <= s["cycles"] for iv in j["intervals"])
