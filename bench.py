@@ -463,45 +463,26 @@ def run_ours(args):
 def bench_attention_vs_lib(ws, torch, dev, stream):
     """Context, not part of `value`: our FA forward next to NVIDIA's trtllm-gen Blackwell FMHA
     (flashinfer's prebuilt sm_100a cubins; library code, like cuBLAS for the GEMM) on the C4/C5
-    hdim-128 S=16K cases, alternating windows on this box (scripts/attn_vs_lib.py has more cases)."""
+    hdim-128 S=16K cases, alternating windows on this box. Run as a bounded subprocess
+    (scripts/attn_vs_lib.py): a library JIT or failure cannot stall or take down the bench."""
+    env = dict(os.environ, CASES="0,1", CUDA_VISIBLE_DEVICES=os.environ.get("CUDA_VISIBLE_DEVICES", str(dev.index or 0)))
     try:
-        import flashinfer  # noqa: F401
-        from scripts.attn_vs_lib import lib_arm
+        out = subprocess.run([sys.executable, os.path.join(ROOT, "scripts", "attn_vs_lib.py")], env=env,
+                             capture_output=True, text=True, timeout=240)
+        line = [l for l in out.stdout.splitlines() if l.startswith("{")]
+        if not line:
+            return {"unavailable": (out.stderr.strip().splitlines() or ["no output"])[-1][:160]}
+        j = json.loads(line[-1])
+        res = {"_method": j.get("_method", "")}
+        names = {"B1_H16_S16384_d128_nc_bf16": "c4_noncausal_s16k_d128", "B1_H16_S16384_d128_c_bf16": "c5_causal_s16k_d128"}
+        for k, v in j.get("attn_vs_trtllm_gen", {}).items():
+            res[names.get(k, k)] = {kk: v[kk] for kk in ("ours_tflops", "lib_tflops", "max_abs_err_vs_fp64") if kk in v} \
+                if "ours_tflops" in v else v
+        return res
+    except subprocess.TimeoutExpired:
+        return {"unavailable": "timed out after 240 s"}
     except Exception as e:  # noqa: BLE001
         return {"unavailable": f"{type(e).__name__}: {str(e)[:120]}"}
-    res = {"_method": "alternating windows (0.3 s apart) of 10 launches, medians of 5; trtllm-gen ragged "
-                      "context FMHA, separate Q/K/V, LSE returned (as ours)"}
-    for name, causal in (("c4_noncausal_s16k_d128", False), ("c5_causal_s16k_d128", True)):
-        try:
-            q = torch.randn(1, 16, 16384, 128, device=dev, dtype=torch.bfloat16)
-            k, v = torch.randn_like(q), torch.randn_like(q)
-            o = torch.empty_like(q)
-            lse = torch.empty(1, 16, 16384, device=dev)
-            ours = lambda: ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse)
-            lib, _ = lib_arm(q, k, v, causal)
-            ours(); lib()
-            torch.cuda.synchronize()
-
-            def window(fn):
-                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-                e0.record(stream)
-                for _ in range(10):
-                    fn()
-                e1.record(stream)
-                torch.cuda.synchronize()
-                return e0.elapsed_time(e1) / 10
-            to, tl = [], []
-            for _ in range(5):
-                time.sleep(0.3)
-                to.append(window(ours))
-                time.sleep(0.3)
-                tl.append(window(lib))
-            fl = 4.0 * 16 * 16384 * 16384 * 128 / (2 if causal else 1)
-            mo, ml = sorted(to)[2], sorted(tl)[2]
-            res[name] = {"ours_tflops": round(fl / mo / 1e9, 1), "lib_tflops": round(fl / ml / 1e9, 1)}
-        except Exception as e:  # noqa: BLE001
-            res[name] = {"unavailable": f"{type(e).__name__}: {str(e)[:120]}"}
-    return res
 
 
 def bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier):
