@@ -110,6 +110,11 @@ typedef struct ws_attn_desc {
                                   double-buffers S per Q tile instead (csrc/attn*_sm100.cuh) */
   float scale_q, scale_k, scale_v; /* E4M3 only: per-tensor descales (0 = 1): scores use
                                   scale_q*scale_k*q.k, O = scale_v * P.v / l */
+  float* MX;                   /* optional [B, H, S] fp32: the exact row max m of the scaled scores
+                                  (natural units), i.e. the flash .k's stored %m; with LSE it gives
+                                  the .k's row sum l = exp(lse - m) and acc = O * l. NULL = skip */
+  int32_t grid_per_item;       /* 1 = one CTA per work item (RunSpec persistent = false); 0 = the
+                                  persistent grid (one CTA per SM over the work items) */
 } ws_attn_desc;
 
 ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream);
@@ -128,9 +133,11 @@ ws_status ws_attn_fwd_traced(const ws_attn_desc* desc, void* cuda_stream, unsign
  * parameters by name, as host arrays: double for `real`, int64 for `int`; in/out; parameters
  * without a buffer start zeroed. Supported shapes: the gemm.k family (gemm / gemm_large /
  * gemm_batched / gemm_act forms, optional 1x1 scale epilogue) — exact for the reference's payloads
- * with device dtype BF16 — and the flash .k of SURVEY.md Appendix A (written back as o = O,
- * lsum = 1, mx = lse, i.e. the same o/lsum and mx + log(lsum) as the .k). Anything else returns
- * WS_UNSUPPORTED_KERNEL; grammar errors WS_PARSE. Synchronous w.r.t. the host buffers. */
+ * with device dtype BF16 — the flash .k of SURVEY.md Appendix A (its three outputs as the .k
+ * defines them: o = the un-normalised accumulator acc, lsum = the row sum l and mx = the running
+ * max m, within the attention tolerances) and the integer max-shift attention.k
+ * (ref proj/kernels/attention.k:1-21, exact in fp16). Anything else returns WS_UNSUPPORTED_KERNEL;
+ * grammar errors WS_PARSE. Synchronous w.r.t. the host buffers. */
 typedef struct ws_kbuffer {
   const char* name;
   int64_t rows, cols;
@@ -140,6 +147,36 @@ typedef struct ws_kbuffer {
 
 ws_status ws_run_kernel(const char* ktext, ws_kbuffer* buffers, int32_t nbuffers, int64_t pid_lo, int64_t pid_hi,
                         int32_t dtype, void* cuda_stream);
+
+/* RunSpec of the reference (ref proj/include/warpspec/driver.hpp:42-57) for a `.k` run on the GPU.
+ * mode: pipeline mode as parse_pipeline_mode (driver.hpp:34-40). Rejections are the reference's,
+ * evaluated on the .k graph before any device work:
+ *   d < 1, p < 1                                   -> PIPELINE_INFEASIBLE (driver.hpp:117-118)
+ *   fine on a loop body that is not a pure dot chain (gemm_act, flash) -> PIPELINE_INFEASIBLE
+ *                                                     (ref pipeline.hpp:57-75)
+ *   fine (or auto on a dot-only body) with p > d   -> PIPELINE_INFEASIBLE (ref pipeline.hpp:84-92)
+ *   coarse on a body without a transform stage     -> PIPELINE_INFEASIBLE (ref pipeline.hpp:264-267)
+ *   coarse with d < 2                              -> PIPELINE_INFEASIBLE (ref pipeline.hpp:309-315);
+ *                                                     auto degrades to plain warp specialization
+ *                                                     (driver.hpp:137-150) and runs
+ *   coop_wgs < 1, or .k output-tile rows % coop_wgs -> INDIVISIBLE_TILE (ref grid.hpp:26-46)
+ * Mapping onto the B200 kernels: d = aref depth (GEMM smem ring; attention K/V ring, min 2 — the
+ * plain warp-specialized and `none` programs run with the smallest ring), p = MMA k-blocks in
+ * flight (GEMM), mode none = d = p = 1 for GEMM, coop_wgs >= 2 = 256-row CTA-pair tiles
+ * (cta_group::2; attention always runs two 128-row Q bands per CTA), persistent = persistent grid.
+ * d = 0 / p = 0 select the library's measured defaults instead of the reference's (2, 1). */
+typedef enum ws_pipeline_mode { WS_MODE_AUTO = 0, WS_MODE_FINE = 1, WS_MODE_COARSE = 2, WS_MODE_NONE = 3 } ws_pipeline_mode;
+typedef struct ws_runspec {
+  int32_t d;
+  int32_t p;
+  int32_t mode;
+  int32_t coop_wgs;
+  int32_t persistent;
+} ws_runspec;
+
+/* ws_run_kernel with a RunSpec (NULL = library defaults: the fastest measured configuration). */
+ws_status ws_run_kernel_spec(const char* ktext, ws_kbuffer* buffers, int32_t nbuffers, int64_t pid_lo,
+                             int64_t pid_hi, int32_t dtype, const ws_runspec* spec, void* cuda_stream);
 
 /* Message for the last non-OK status returned on this thread ("" if none). */
 const char* ws_last_error(void);

@@ -34,6 +34,20 @@ struct Launch {
   int64_t pid_hi = 1;
   int32_t dtype = WS_BF16; // device storage type of the real payloads (exact for the reference's)
   void* stream = nullptr;  // cudaStream_t; the call is synchronous w.r.t. the host buffers
+  // the reference's RunSpec knobs (ref proj/include/warpspec/driver.hpp:42-57), validated with
+  // compile_kernel's rejections; unset = the library's measured defaults
+  bool use_spec = false;
+  ws_runspec spec{0, 0, WS_MODE_AUTO, 0, 1};
+  // from a reference RunSpec: d, p, mode, coop_wgs, persistent (tiles / paths stay the caller's)
+  template <class RunSpecT>
+  void set_spec(const RunSpecT& rs) {
+    use_spec = true;
+    spec.d = rs.d;
+    spec.p = rs.p;
+    spec.mode = static_cast<int32_t>(rs.mode);  // PipelineMode order: Auto, Fine, Coarse, None
+    spec.coop_wgs = rs.coop_wgs;
+    spec.persistent = rs.persistent ? 1 : 0;
+  }
 };
 
 inline void check(ws_status s) {
@@ -69,8 +83,8 @@ inline warpspec::Buffers run_graph(const warpspec::KernelGraph& g, const std::st
     b.data = b.is_real ? static_cast<void*>(t.rv.data()) : static_cast<void*>(t.iv.data());
     bufs.push_back(b);
   }
-  check(ws_run_kernel(ktext.c_str(), bufs.data(), static_cast<int32_t>(bufs.size()), launch.pid_lo, launch.pid_hi,
-                      launch.dtype, launch.stream));
+  check(ws_run_kernel_spec(ktext.c_str(), bufs.data(), static_cast<int32_t>(bufs.size()), launch.pid_lo,
+                           launch.pid_hi, launch.dtype, launch.use_spec ? &launch.spec : nullptr, launch.stream));
   return out;
 }
 }  // namespace detail

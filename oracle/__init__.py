@@ -141,6 +141,33 @@ def flash(q: np.ndarray, k: np.ndarray, v: np.ndarray, causal: bool, softmax_sca
     return o.reshape(shape), lse.reshape(shape[:-1])
 
 
+def flash_stats(q: np.ndarray, k: np.ndarray, causal: bool, softmax_scale: float | None = None) -> np.ndarray:
+    """The flash .k's stored running max m (ref: the `%mn` chain of SURVEY App. A): the row max of
+    the scaled scores, causal positions above the diagonal excluded. [BH, S, Dh] -> [BH, S]."""
+    q = np.asarray(q, dtype=np.float64)
+    k = np.asarray(k, dtype=np.float64)
+    S, Dh = q.shape[-2], q.shape[-1]
+    sc = softmax_scale if softmax_scale is not None else 1.0 / np.sqrt(Dh)
+    s = np.einsum("bqd,bkd->bqk", q.reshape(-1, S, Dh), k.reshape(-1, S, Dh)) * sc
+    if causal:
+        s = np.where(np.tril(np.ones((S, S), dtype=bool)), s, -np.inf)
+    return s.max(axis=-1)
+
+
+def maxshift(q: np.ndarray, kt: np.ndarray, v: np.ndarray, D: int) -> np.ndarray:
+    """The shipped max-shift attention.k (ref proj/kernels/attention.k:1-21) over all its pids, in
+    exact int64: per key block j (kt[0:D, jD:(j+1)D], v[jD:(j+1)D]) s = q . tk^T,
+    acc += (s - rowmax s) . tv (ref tile.hpp eval_dot / eval_reduce / eval_ew_binary)."""
+    q = np.asarray(q, dtype=np.int64)
+    kt = np.asarray(kt, dtype=np.int64)
+    v = np.asarray(v, dtype=np.int64)
+    o = np.zeros((q.shape[0], v.shape[1]), dtype=np.int64)
+    for j in range(kt.shape[1] // D):
+        s = q[:, :D] @ kt[:D, j * D:(j + 1) * D].T
+        o += (s - s.max(axis=1, keepdims=True)) @ v[j * D:(j + 1) * D]
+    return o
+
+
 # ----------------------------------------------------------------------------------------------
 # the reference itself (oracle/_ref/libwsref.so)
 # ----------------------------------------------------------------------------------------------

@@ -228,3 +228,41 @@ def gemm_act_src(M: int, N: int, K: int, BM: int, BN: int, BK: int, elem: str = 
         "  store c[%r, %cn] = %last",
         "}",
     ]) + "\n"
+
+
+def shipped(name: str, root: str = "/root/reference/proj/kernels") -> str:
+    """A `.k` file shipped with the reference, verbatim (golden generation only: /root/reference
+    exists in the build container, not on the GPU box; the text is stored in the golden)."""
+    with open(f"{root}/{name}") as f:
+        return f.read()
+
+
+def maxshift_src(R: int, D: int, S: int, BR: int, DV: int | None = None, elem: str = "int") -> str:
+    """The shipped max-shift attention.k (ref proj/kernels/attention.k:1-21) at other sizes: q R x D,
+    kt D x S, v S x DV, o R x DV; pid = query block of BR rows; iteration j takes the D x D key tile
+    kt[0, j*D] and the D x DV value tile v[j*D, 0] (the shipped file is R=32, D=8, S=64, BR=8)."""
+    DV = DV or D
+    assert R % BR == 0 and S % D == 0
+    return "\n".join([
+        f"kernel attention(q: buf<{R}x{D} {elem}>, kt: buf<{D}x{S} {elem}>, v: buf<{S}x{DV} {elem}>, "
+        f"o: buf<{R}x{DV} {elem}>) {{",
+        "  %p = pid",
+        f"  %r = mul %p, {BR}",
+        f"  %zs = const zeros : {BR}x{D} {elem}",
+        f"  %zacc = const zeros : {BR}x{DV} {elem}",
+        "  %k0 = const 0",
+        f"  loop %k in 0..{S // D} iter (%acc = %zacc, %ok = %k0) {{",
+        f"    %tq = tma_load q[%r, 0] : {BR}x{D} {elem}",
+        f"    %tk = tma_load kt[0, %ok] : {D}x{D} {elem}",
+        f"    %tv = tma_load v[%ok, 0] : {D}x{DV} {elem}",
+        "    %s = dot %tq, %tk.T, acc=%zs",
+        "    %m = reduce max %s axis=1",
+        "    %sub = ew sub %s, %m",
+        "    %acc1 = dot %sub, %tv, acc=%acc",
+        f"    %ok1 = add %ok, {D}",
+        "    yield %acc1, %ok1",
+        "  }",
+        "  store o[%r, 0] = %acc",
+        "}",
+        "",
+    ])

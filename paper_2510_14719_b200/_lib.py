@@ -50,6 +50,8 @@ class AttnDesc(ctypes.Structure):
         ("bh_begin", ctypes.c_int32), ("bh_end", ctypes.c_int32),
         ("kv_block", ctypes.c_int32),
         ("scale_q", ctypes.c_float), ("scale_k", ctypes.c_float), ("scale_v", ctypes.c_float),
+        ("MX", ctypes.c_void_p),
+        ("grid_per_item", ctypes.c_int32),
     ]
 
 
@@ -60,6 +62,15 @@ class KBuffer(ctypes.Structure):
         ("is_real", ctypes.c_int32),
         ("data", ctypes.c_void_p),
     ]
+
+
+class RunSpec(ctypes.Structure):
+    """Mirror of ws_runspec (include/ws.h): the reference's RunSpec (ref driver.hpp:42-57)."""
+    _fields_ = [("d", ctypes.c_int32), ("p", ctypes.c_int32), ("mode", ctypes.c_int32),
+                ("coop_wgs", ctypes.c_int32), ("persistent", ctypes.c_int32)]
+
+
+MODES = {"auto": 0, "fine": 1, "coarse": 2, "none": 3}  # ref driver.hpp:34-40 parse_pipeline_mode
 
 
 # every symbol include/ws.h declares, with its ctypes signature
@@ -78,6 +89,8 @@ EXPORTS = {
     "ws_watchdog": (ctypes.c_int32, [ctypes.c_void_p]),
     "ws_run_kernel": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(KBuffer), ctypes.c_int32, ctypes.c_int64,
                                      ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]),
+    "ws_run_kernel_spec": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(KBuffer), ctypes.c_int32, ctypes.c_int64,
+                                          ctypes.c_int64, ctypes.c_int32, ctypes.POINTER(RunSpec), ctypes.c_void_p]),
     "ws_last_error": (ctypes.c_char_p, []),
     "ws_launch_count": (ctypes.c_int64, []),
     "ws_version": (ctypes.c_char_p, []),

@@ -50,6 +50,7 @@ struct Attn128Params {
   float scale_log2;   // softmax_scale * log2(e) (* q, k descales for FP8)
   float o_scale;      // V descale folded into the epilogue (1 unless FP8)
   float* lse;
+  float* mx;          // optional: exact row max of the scaled scores (natural units; the .k's %m)
   void* o;
   unsigned long long* trace;  // optional %clock64 stamps of CTA (0,0), layout of attn_sm100.cuh
 };
@@ -294,6 +295,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     const int q_row0 = bh * p.S + pair * 2 * A128_BM;
     const int j_diag = p.causal ? n_t - 1 : -1;
     float m_used = -INFINITY;  // running max (log2 units) the current P/O are relative to
+    float m_true = -INFINITY;  // exact running row max (log2 units; the .k's %m, for p.mx)
     float l = 0.f;
     for (int j = 0; j < n_t; ++j) {
       if (tr) WS_TRACE(1 + t, j, 0);
@@ -328,6 +330,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
       }
       const float m_blk = mx * sl2;
+      m_true = fmaxf(m_true, m_blk);
       float alpha = 1.f;
       const bool need = m_blk > m_used + ATTN_RESCALE_THRESHOLD;
       if (need) {
@@ -421,6 +424,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       *reinterpret_cast<uint4*>(orow + c0 * 2) = make_uint4(w[0], w[1], w[2], w[3]);
     }
     if (p.lse) p.lse[grow] = m_used * 0.69314718055994531f + __logf(l);
+    if (p.mx) p.mx[grow] = m_true * 0.69314718055994531f;
     }  // items
   }
 

@@ -332,6 +332,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     const bool tile_valid = (2 * pair + t) * A128_BM < p.S;
     const int j_diag = p.causal ? n_t - 1 : -1;
     float m_used = -INFINITY;  // running max (log2 units) the current P/O are relative to
+    float m_true = -INFINITY;  // exact running row max (log2 units; the .k's %m, for p.mx)
     float l = 0.f;
     for (int j = 0; j < n_t; ++j) {
       if (tr) WS_TRACE(1 + t, g + j, 0);
@@ -385,6 +386,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
       }
       const float m_blk = mx * sl2;
+      m_true = fmaxf(m_true, m_blk);
       float alpha = 1.f;
       const bool need = m_blk > m_used + ATTN_RESCALE_THRESHOLD;
       if (need) {
@@ -521,6 +523,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       }
     }
     if (p.lse && tile_valid) p.lse[grow] = m_used * 0.69314718055994531f + __logf(l);
+    if (p.mx && tile_valid) p.mx[grow] = m_true * 0.69314718055994531f;
     if (tr) WS_TRACE(1 + t, g - 1, 7);
     }  // items
     if (warp == 4u * t && lane == 0) tma_store_wait<0>();  // O stores complete before the CTA retires

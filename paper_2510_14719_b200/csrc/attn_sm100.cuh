@@ -51,6 +51,7 @@ struct AttnParams {
   int causal;
   float scale_log2;  // softmax_scale * log2(e)
   float* lse;
+  float* mx;  // optional: exact row max of the scaled scores (natural units; the .k's %m)
   void* o;
   int o_elem;  // 0 = bf16, 1 = f16
   // optional device trace (ws_attn_fwd_traced): %clock64 stamps of CTA (0,0), see ATTN_TRACE_*
@@ -272,6 +273,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
     const int qpos = tile_q0 + row;  // query position in the sequence
     const float sl2 = p.scale_log2;
     float m_used = -INFINITY;  // running max (log2 units) the current P/O are relative to
+    float m_true = -INFINITY;  // exact running row max (log2 units; the .k's %m, for p.mx)
     float l = 0.f;
     const bool tr = lane == 0 && (warp & 3u) == 0;
     for (int j = 0; j < n_kv; ++j) {
@@ -307,6 +309,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
         mx = fmaxf(fmaxf(m4[0], m4[1]), fmaxf(m4[2], m4[3]));
       }
       const float m_blk = mx * sl2;
+      m_true = fmaxf(m_true, m_blk);
       float alpha = 1.f;
       const bool need = m_blk > m_used + ATTN_RESCALE_THRESHOLD;
       if (need) {
@@ -399,6 +402,7 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
       for (int e = 0; e < 4; ++e) dst[e] = make_uint4(w[4 * e], w[4 * e + 1], w[4 * e + 2], w[4 * e + 3]);
     }
     if (p.lse) p.lse[grow] = m_used * 0.69314718055994531f + __logf(l);
+    if (p.mx) p.mx[grow] = m_true * 0.69314718055994531f;
   }
 
   tc_fence_before();

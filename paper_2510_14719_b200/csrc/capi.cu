@@ -40,6 +40,7 @@ ws_status fail(ws_status s, const std::string& msg) {
 
 namespace ws_detail {
 ws_status set_error(ws_status s, const std::string& m) { return fail(s, m); }
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 }  // namespace ws_detail
 
 namespace {
@@ -137,28 +138,52 @@ ws_status make_tmap_uncached(CUtensorMap* m, const void* ptr, int dt, int64_t ro
   return WS_OK;
 }
 
+// Per-device state. Everything a launch needs from the device context — SM count, the dynamic
+// shared-memory opt-in of each kernel, the wait-hint / watchdog symbols — is set per device
+// ordinal (one process may drive several GPUs; the launch's current device is the stream's).
+constexpr int MAX_DEVICES = 64;
+
+int current_device() {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return dev < 0 || dev >= MAX_DEVICES ? 0 : dev;
+}
+
 int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+  static std::atomic<int> n[MAX_DEVICES];
+  const int dev = current_device();
+  int v = n[dev].load(std::memory_order_relaxed);
+  if (v == 0) {
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    n[dev].store(v, std::memory_order_relaxed);
   }
-  return n;
+  return v;
 }
 
 constexpr int SMEM_LIMIT = 232448;  // 227 KB opt-in per CTA on sm_100a
 
-// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per kernel and size (it costs a driver
-// call per launch otherwise; small GEMMs are launch-bound)
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) once per (device, kernel) and size (it costs a
+// driver call per launch otherwise; small GEMMs are launch-bound). Lock-free: a per-thread table
+// (a thread that has not seen the pair yet repeats the idempotent attribute call once).
 cudaError_t allow_smem(const void* kern, int bytes) {
-  static std::mutex mu;
-  static std::unordered_map<const void*, int> done;
-  std::lock_guard<std::mutex> g(mu);
-  auto it = done.find(kern);
-  if (it != done.end() && it->second >= bytes) return cudaSuccess;
+  struct Entry {
+    const void* kern;
+    int dev, bytes;
+  };
+  thread_local Entry done[64];
+  thread_local int n = 0;
+  const int dev = current_device();
+  for (int i = 0; i < n; ++i)
+    if (done[i].kern == kern && done[i].dev == dev && done[i].bytes >= bytes) return cudaSuccess;
   const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) done[kern] = bytes;
+  if (e == cudaSuccess) {
+    for (int i = 0; i < n; ++i)
+      if (done[i].kern == kern && done[i].dev == dev) {
+        done[i].bytes = bytes;
+        return e;
+      }
+    done[n < 64 ? n++ : 63] = Entry{kern, dev, bytes};
+  }
   return e;
 }
 
@@ -166,29 +191,39 @@ cudaError_t allow_smem(const void* kern, int bytes) {
 // the barrier (woken when the phase completes) instead of re-issuing try_wait, which leaves the
 // issue slots to the softmax warps sharing its SM sub-partition (hdim-64 causal attention +5-10%,
 // GEMM unchanged; scripts/attn_ab.py). WS_WAIT_HINT_NS overrides (0 = hardware default). Set once
-// per device context before the first launch.
-ws::WatchdogRecord* g_watchdog_host = nullptr;  // pinned, mapped: survives a trapped context
+// per device context before its first launch.
+ws::WatchdogRecord* g_watchdog_host = nullptr;  // pinned, mapped, portable: survives a trapped context
 
 void apply_wait_hint() {
-  static std::once_flag once;
-  std::call_once(once, [] {
+  static std::once_flag once[MAX_DEVICES];
+  static std::once_flag host_once;
+  const int dev = current_device();
+  std::call_once(once[dev], [] {
     const char* e = getenv("WS_WAIT_HINT_NS");
     const uint32_t ns = e ? static_cast<uint32_t>(atoi(e)) : 200000u;
     cudaMemcpyToSymbol(ws::ws_wait_hint_ns, &ns, sizeof(ns));
-    // the watchdog's host-mapped record (ws_watchdog)
-    void* h = nullptr;
-    cudaError_t e1 = cudaHostAlloc(&h, sizeof(ws::WatchdogRecord), cudaHostAllocMapped), e2 = cudaErrorUnknown,
-                e3 = cudaErrorUnknown;
+    // the watchdog's host-mapped record (ws_watchdog): one portable allocation, its device
+    // address written into each device's copy of the module symbol
+    std::call_once(host_once, [] {
+      void* h = nullptr;
+      if (cudaHostAlloc(&h, sizeof(ws::WatchdogRecord), cudaHostAllocMapped | cudaHostAllocPortable) == cudaSuccess) {
+        std::memset(h, 0, sizeof(ws::WatchdogRecord));
+        g_watchdog_host = static_cast<ws::WatchdogRecord*>(h);
+      }
+    });
     void* d = nullptr;
-    if (e1 == cudaSuccess) {
-      std::memset(h, 0, sizeof(ws::WatchdogRecord));
-      e2 = cudaHostGetDevicePointer(&d, h, 0);
-      if (e2 == cudaSuccess) e3 = cudaMemcpyToSymbol(ws::ws_watchdog_host, &d, sizeof(d));
-      if (e3 == cudaSuccess) g_watchdog_host = static_cast<ws::WatchdogRecord*>(h);
-    }
-
+    if (g_watchdog_host && cudaHostGetDevicePointer(&d, g_watchdog_host, 0) == cudaSuccess)
+      cudaMemcpyToSymbol(ws::ws_watchdog_host, &d, sizeof(d));
   });
 }
+
+// developer knobs, read once per process
+int env_int(const char* name, int dflt) {
+  const char* e = getenv(name);
+  return e ? atoi(e) : dflt;
+}
+const int g_debug_deadlock = env_int("WS_DEBUG_DEADLOCK", 0);
+const bool g_trace_global = getenv("WS_GEMM_TRACE_GLOBAL") != nullptr;
 
 unsigned long long* g_gemm_trace = nullptr;  // ws_debug_gemm_trace
 
@@ -229,9 +264,8 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   p.trace = g_gemm_trace;
   // developer diagnostics: WS_DEBUG_DEADLOCK=1 makes CTA 0's producer skip its first aref put, so
   // the MMA warp waits forever and the watchdog fires (the simulator's Deadlock verdict on hardware)
-  static const int deadlock_env = getenv("WS_DEBUG_DEADLOCK") ? atoi(getenv("WS_DEBUG_DEADLOCK")) : 0;
-  p.debug_deadlock = deadlock_env;
-  p.trace_global = getenv("WS_GEMM_TRACE_GLOBAL") != nullptr;
+  p.debug_deadlock = g_debug_deadlock;
+  p.trace_global = g_trace_global;
 
   CUtensorMap ta, tb, tc;
   ws_status s;
@@ -324,6 +358,7 @@ ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stre
   const float sm = d.softmax_scale > 0.f ? d.softmax_scale : 1.0f / std::sqrt((float)DH);
   p.scale_log2 = sm * 1.4426950408889634f;
   p.lse = d.LSE;
+  p.mx = d.MX;
   p.o = d.O;
   p.o_elem = BF16 ? 0 : 1;
   p.trace = trace;
@@ -379,6 +414,7 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
   p.scale_log2 = sm * 1.4426950408889634f;
   p.o_scale = 1.f;
   p.lse = d.LSE;
+  p.mx = d.MX;
   p.o = d.O;
   p.trace = trace;
   auto smem_bytes = [](int stages) { return PSMEM ? aps_smem_bytes(DH, stages) : a128_smem_bytes(DH, stages); };
@@ -429,7 +465,7 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
       return e ? atoi(e) : 1;
     }();
     const int items = p.num_pairs * p.num_bh;
-    cfg.gridDim = dim3(persist_env == 0 || items < num_sms() ? items : num_sms());
+    cfg.gridDim = dim3(persist_env == 0 || d.grid_per_item || items < num_sms() ? items : num_sms());
   }
   cfg.blockDim = dim3(A128_THREADS);
   cfg.dynamicSmemBytes = smem;
@@ -460,6 +496,7 @@ ws_status launch_attn_fp8(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t 
   p.scale_log2 = sm * sq * sk * 1.4426950408889634f;
   p.o_scale = sv;
   p.lse = d.LSE;
+  p.mx = d.MX;
   p.o = d.O;
   p.trace = trace;
   const uint32_t kvb = A128_BN * DH;  // one e4m3 K or V block
@@ -504,7 +541,7 @@ ws_status launch_attn_fp8(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t 
   WS_CUDA_CHECK(allow_smem(reinterpret_cast<const void*>(kern), (int)smem));
   cudaLaunchConfig_t cfg = {};
   const int items = p.num_pairs * p.num_bh;
-  cfg.gridDim = dim3(items < num_sms() ? items : num_sms());
+  cfg.gridDim = dim3(d.grid_per_item || items < num_sms() ? items : num_sms());
   cfg.blockDim = dim3(A128_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
@@ -623,9 +660,11 @@ ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
   const double cost256 = (double)((t256 + pairs - 1) / pairs) * 712.0;
   const bool fill512 = cost512 <= cost256;
   const bool fill256 = nbat * (d.M / 128) * (d.N / 256) >= units;
+  // (N a multiple of 128 but not of 256: 128-wide tiles, single CTA or pair)
   int bn = d.bn > 0 ? d.bn
            : (d.cta_pair && kblocks >= 16 && d.N % 512 == 0 && fill512) ? 512
            : (!d.cta_pair && !fill256 && d.N % 128 == 0)                 ? 128
+           : (d.N % 256 != 0 && d.N % 128 == 0)                          ? 128
                                                                          : 256;
   if (bn != 128 && bn != 256 && bn != 512) return fail(WS_TYPE, "bn must be 128, 256 or 512");
   if (bn == 512 && !d.cta_pair) return fail(WS_TYPE, "bn=512 (256 x 512 tiles) needs cta_pair=1");

@@ -12,8 +12,12 @@
 //   3. runs the tile math as tensor-core launches through the C-ABI:
 //      gemm.k family (gemm.k / gemm_large.k / gemm_batched.k / gemm_act.k shapes, optional
 //      1x1 scale or relu epilogue) -> pids grouped into zero-padded ws_gemm_tn launches;
-//      flash .k of SURVEY.md Appendix A -> ws_attn_fwd.
+//      flash .k of SURVEY.md Appendix A -> ws_attn_fwd (acc, l and m written back as the .k's);
+//      max-shift attention.k (ref proj/kernels/attention.k) -> GEMM, row-block shift, GEMM.
+//   4. applies a RunSpec (ws_runspec, ref driver.hpp:42-57) with compile_kernel's rejections.
 // Unsupported shapes fail with WS_UNSUPPORTED_KERNEL, never with a CPU fallback.
+#include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -25,9 +29,15 @@
 #include <set>
 #include <stdexcept>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/ws.h"
+
+namespace ws_detail {
+ws_status set_error(ws_status s, const std::string& m);  // capi.cu
+void count_launch();                                       // capi.cu: ws_launch_count evidence
+}  // namespace ws_detail
 
 namespace {
 
@@ -503,8 +513,99 @@ struct ScalarEnv {
   }
 };
 
+
 // ------------------------------------------------------------------------------------------------
-// host buffers
+// RunSpec -> launch choices (ref proj/include/warpspec/driver.hpp:42-57, compile_kernel :116-189)
+// ------------------------------------------------------------------------------------------------
+struct Plan {
+  int d = 0, p = 0;         // aref depth / MMA k-blocks in flight on the GPU; 0 = library default
+  int coop = 0;             // 0 = library default, 1 = single-CTA tiles, 2 = CTA-pair tiles
+  bool persistent = true;
+  std::string mode;         // the pipeline the reference's compile_kernel applies: none|ws|fine|coarse
+};
+
+// The rejections of compile_kernel, in its order, evaluated on the parsed graph: D/P range
+// (driver.hpp:117-118), the pipelining pass (fine: pipeline.hpp:44-92; coarse: :258-315; auto:
+// driver.hpp:129-150), then the cooperative split (grid.hpp:24-46). The reference's register and
+// shared-memory gates are cost-model conventions; the kernels apply the real
+// sm_100a limits at launch.
+Plan resolve_spec(const Kernel& g, const ws_runspec* rs) {
+  Plan pl;
+  if (!rs) {
+    pl.mode = "auto";
+    return pl;
+  }
+  if (rs->d < 0) kfail(WS_PIPELINE_INFEASIBLE, "D must be >= 1");
+  if (rs->p < 0) kfail(WS_PIPELINE_INFEASIBLE, "P must be >= 1");
+  if (rs->mode < WS_MODE_AUTO || rs->mode > WS_MODE_NONE) kfail(WS_PARSE, "unknown pipeline mode");
+  pl.d = rs->d;
+  pl.p = rs->p;
+  pl.persistent = rs->persistent != 0;
+  bool has_t = false, has_c = false, axis0 = false;
+  for (const Op& o : g.body) {
+    if (o.k == K::Dot) has_t = true;
+    if (o.k == K::Ew || o.k == K::Reduce) has_c = true;
+    if (o.k == K::Reduce && o.axis == 0) axis0 = true;
+  }
+  const int64_t trip = g.hi - g.lo;
+  if (rs->mode == WS_MODE_NONE) {
+    pl.mode = "none";
+    pl.d = pl.p = 1;  // the sequential program: one stage, one MMA group in flight
+  } else {
+    int mode = rs->mode;
+    const bool autom = mode == WS_MODE_AUTO;
+    if (autom) mode = (has_t && has_c && trip >= 1) ? WS_MODE_COARSE : (has_t && trip >= 1) ? WS_MODE_FINE : -1;
+    pl.mode = "ws";
+    if (mode == WS_MODE_COARSE) {
+      if (trip < 1) kfail(WS_PIPELINE_INFEASIBLE, "coarse-grained schedule needs at least one trip");
+      if (!has_t || !has_c)
+        kfail(WS_PIPELINE_INFEASIBLE, "coarse-grained schedule needs a tensor-core stage and a transform stage");
+      if (pl.d == 1) {
+        if (!autom) kfail(WS_PIPELINE_INFEASIBLE, "coarse-grained schedule needs channel depth D >= 2");
+        // auto: a staged schedule that does not fit degrades to plain warp specialization
+      } else {
+        pl.mode = "coarse";
+      }
+      pl.p = 0;  // no MMA window in a coarse schedule: commits release the stages
+    } else if (mode == WS_MODE_FINE) {
+      if (has_c) kfail(WS_PIPELINE_INFEASIBLE, "fine-grained pipelining needs a pure dot-chain loop body");
+      if (!has_t) kfail(WS_PIPELINE_INFEASIBLE, "fine-grained pipelining needs at least one dot");
+      if (pl.d > 0 && pl.p > pl.d)
+        kfail(WS_PIPELINE_INFEASIBLE, "P=" + std::to_string(pl.p) + " exceeds channel depth D=" + std::to_string(pl.d) +
+                                          " (deadlock: a slot would be reused while borrowed)");
+      pl.mode = "fine";
+    } else {
+      pl.p = 0;
+    }
+  }
+  if (rs->coop_wgs < 0) kfail(WS_INDIVISIBLE_TILE, "cooperative warp group count must be >= 1");
+  if (rs->coop_wgs > 1) {
+    if (axis0) kfail(WS_INDIVISIBLE_TILE, "row-band split cannot cross an axis-0 reduction");
+    for (const Op& o : g.epi)
+      if (o.k == K::Store) {
+        const Op* src = nullptr;
+        for (auto* ops : {&g.epi, &g.body, &g.pro})
+          for (const Op& x : *ops)
+            if (x.res == o.args[0]) src = &x;
+        int64_t rows = src ? src->shape.r : 0;
+        if (!src) {  // an iter arg: its init's tile shape
+          for (auto& [a, init] : g.iter)
+            if (a == o.args[0])
+              for (auto* ops : {&g.pro})
+                for (const Op& x : *ops)
+                  if (x.res == init) rows = x.shape.r;
+        }
+        if (rows > 0 && rows % rs->coop_wgs != 0)
+          kfail(WS_INDIVISIBLE_TILE, "output tile rows " + std::to_string(rows) + " not divisible by " +
+                                         std::to_string(rs->coop_wgs) + " warp groups");
+      }
+  }
+  pl.coop = rs->coop_wgs == 0 ? 0 : rs->coop_wgs == 1 ? 1 : 2;
+  return pl;
+}
+
+// ------------------------------------------------------------------------------------------------
+// host buffers, staging
 // ------------------------------------------------------------------------------------------------
 struct HostBuf {
   std::string name;
@@ -521,6 +622,12 @@ struct HostBuf {
       static_cast<double*>(data)[i] = x;
     else
       static_cast<int64_t*>(data)[i] = static_cast<int64_t>(std::llround(x));
+  }
+  double amax() const {
+    double m = 0;
+    const int64_t n = shape.r * shape.c;
+    for (int64_t i = 0; i < n; ++i) m = std::max(m, std::fabs(get(i / shape.c, i % shape.c)));
+    return m;
   }
 };
 
@@ -552,17 +659,87 @@ uint16_t to_half_bits(float f, int dt) {
   return static_cast<uint16_t>(sign | half);
 }
 
-struct DevBuf {
-  void* p = nullptr;
-  ~DevBuf() {
-    if (p) cudaFree(p);
+float half_to_float(uint16_t h, int dt) {
+  uint32_t u;
+  if (dt == WS_BF16) {
+    u = static_cast<uint32_t>(h) << 16;
+  } else {
+    const uint32_t s = (h & 0x8000u) << 16, e = (h >> 10) & 0x1F, m = h & 0x3FF;
+    if (e == 0) {
+      float f = std::ldexp(static_cast<float>(m), -24);
+      return s ? -f : f;
+    }
+    u = s | ((e + 112) << 23) | (m << 13);
   }
-};
+  float f;
+  std::memcpy(&f, &u, 4);
+  return f;
+}
+
 void cuda_check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) kfail(WS_CUDA_ERROR, std::string(what) + ": " + cudaGetErrorString(e));
 }
 void ws_check(ws_status s) {
   if (s != WS_OK) kfail(s, ws_last_error());
+}
+
+// Per host thread: device blocks and pinned host blocks reused across calls (a .k run is
+// synchronous, so a block is free again when the call returns), grown on demand.
+struct Staging {
+  struct Blk {
+    void* p = nullptr;
+    size_t n = 0;
+    int dev = -1;
+  };
+  Blk dev[8], host[8];
+  void* device(int i, size_t n) {
+    int cur = 0;
+    cudaGetDevice(&cur);
+    Blk& b = dev[i];
+    if (b.n < n || b.dev != cur) {
+      if (b.p) cudaFree(b.p);
+      b = Blk{};
+      cuda_check(cudaMalloc(&b.p, n), "cudaMalloc");
+      b.n = n;
+      b.dev = cur;
+    }
+    return b.p;
+  }
+  void* pinned(int i, size_t n) {
+    Blk& b = host[i];
+    if (b.n < n) {
+      if (b.p) cudaFreeHost(b.p);
+      b = Blk{};
+      cuda_check(cudaHostAlloc(&b.p, n, cudaHostAllocPortable), "cudaHostAlloc");
+      b.n = n;
+    }
+    return b.p;
+  }
+  ~Staging() {
+    for (Blk& b : dev)
+      if (b.p) cudaFree(b.p);
+    for (Blk& b : host)
+      if (b.p) cudaFreeHost(b.p);
+  }
+};
+thread_local Staging g_stage;
+
+// Host conversion loops over rows [0, n), split over host threads when large.
+template <class F>
+void parallel_rows(int64_t n, int64_t work_per_row, F&& f) {
+  const int64_t work = n * std::max<int64_t>(1, work_per_row);
+  int nt = static_cast<int>(std::min<int64_t>(std::thread::hardware_concurrency(), 16));
+  if (work < (int64_t(1) << 20) || nt <= 1 || n < 2) {
+    for (int64_t i = 0; i < n; ++i) f(i);
+    return;
+  }
+  nt = static_cast<int>(std::min<int64_t>(nt, n));
+  std::vector<std::thread> th;
+  for (int t = 0; t < nt; ++t)
+    th.emplace_back([&, t] {
+      for (int64_t i = n * t / nt; i < n * (t + 1) / nt; ++i) f(i);
+    });
+  for (auto& x : th) x.join();
 }
 
 const Op* def_of(const std::vector<Op>& ops, const std::string& v) {
@@ -591,6 +768,48 @@ std::vector<const Op*> tile_ops(const std::vector<Op>& ops) {
     if (o.k == K::Load || o.k == K::Dot || o.k == K::Ew || o.k == K::Reduce || o.k == K::ConstTile) r.push_back(&o);
   return r;
 }
+const Op* const_1x1(const Kernel& g, const std::string& v) {
+  const Op* c = def_any(g, v);
+  return (c && c->k == K::ConstTile && !c->zeros && c->shape.r == 1 && c->shape.c == 1) ? c : nullptr;
+}
+bool zeros_tile(const Kernel& g, const std::string& v) {
+  const Op* c = def_any(g, v);
+  return c && c->k == K::ConstTile && c->zeros;
+}
+
+// Per-pid scalar state: the prologue run, iter args initialised; step() runs one iteration's
+// body and advances the scalar iter args through the yield.
+struct PidEval {
+  const Kernel& g;
+  ScalarEnv env;
+  PidEval(const Kernel& k, int64_t pid) : g(k) {
+    env.run(g.pro, pid);
+    for (auto& [a, init] : g.iter)
+      if (env.v.count(init)) env.v[a] = env.v[init];
+    pid_ = pid;
+  }
+  ScalarEnv step(int64_t j) {
+    ScalarEnv e2 = env;
+    e2.v[g.ind] = j;
+    e2.run(g.body, pid_);
+    const Op* y = yield_op(g);
+    if (y)
+      for (size_t i = 0; i < g.iter.size() && i < y->args.size(); ++i)
+        if (e2.v.count(y->args[i])) env.v[g.iter[i].first] = e2.v[y->args[i]];
+    return e2;
+  }
+  int64_t pid_;
+};
+
+// int payloads run exactly when every value is exact in the device type and every partial sum
+// of the fp32 accumulation stays below 2^24; the requested 16-bit type is kept when it is exact,
+// else fp16 (integers up to 2048) when that is
+int exact_int_dtype(int dt, double amax_inputs) {
+  const double lim = dt == WS_BF16 ? 256.0 : 2048.0;
+  if (amax_inputs <= lim) return dt;
+  if (amax_inputs <= 2048.0) return WS_F16;
+  kfail(WS_UNSUPPORTED_KERNEL, "int payloads with |x| > 2048 are not exact in a 16-bit tensor-core type");
+}
 
 // ------------------------------------------------------------------------------------------------
 // gemm.k family
@@ -599,7 +818,15 @@ struct PidTile {
   int64_t pid, r0, c0, ra, rb, ka0, kb0;
 };
 
-bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo, int64_t hi, int dt, cudaStream_t st) {
+void gemm_launch_knobs(ws_gemm_desc& d, const Plan& pl, int64_t Kp) {
+  d.D = pl.d;
+  d.P = pl.p;
+  d.persistent = pl.persistent ? 1 : 0;
+  d.cta_pair = pl.coop == 0 ? (Kp >= 1024 ? 1 : 0) : pl.coop == 2 ? 1 : 0;
+}
+
+bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo, int64_t hi, int dt, const Plan& pl,
+              cudaStream_t st) {
   // body: exactly two loads and one dot(a, b.T, acc=<iter arg>), optional relu of the new acc,
   // yield; prologue acc init = zeros; epilogue: store of the acc (or of the relu'd iter arg), or
   // of `ew mul acc, <1x1 const>`
@@ -627,7 +854,6 @@ bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo,
   int relu_i = -1;
   if (relu) {
     if (relu->args[0] != dot->res) return false;
-    relu_i = -1;
     for (size_t i = 0; i < y->args.size(); ++i)
       if (y->args[i] == relu->res) relu_i = static_cast<int>(i);
     if (relu_i < 0) return false;
@@ -651,8 +877,8 @@ bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo,
   std::string stored = store->args[0];
   if (scale_op) {
     if (stored != scale_op->res) return false;
-    const Op* c = def_any(g, scale_op->args[1]);
-    if (!c || c->k != K::ConstTile || c->zeros || c->shape.r != 1 || c->shape.c != 1) return false;
+    const Op* c = const_1x1(g, scale_op->args[1]);
+    if (!c) return false;
     scale = c->lit[0];
     stored = scale_op->args[0];
   }
@@ -675,16 +901,10 @@ bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo,
   // per-pid geometry from the scalar program (and linear K offsets across iterations)
   std::vector<PidTile> tiles;
   for (int64_t pid = lo; pid < hi; ++pid) {
-    ScalarEnv env;
-    env.run(g.pro, pid);
-    std::map<std::string, int64_t> iter_s;
-    for (auto& [a, init] : g.iter)
-      if (env.v.count(init)) env.v[a] = env.v[init];
+    PidEval pe(g, pid);
     int64_t ra = 0, rb = 0, ka = 0, kb = 0, ka1 = 0, kb1 = 0;
     for (int64_t k = g.lo; k < std::min(g.hi, g.lo + 2); ++k) {
-      ScalarEnv e2 = env;
-      e2.v[g.ind] = k;
-      e2.run(g.body, pid);
+      ScalarEnv e2 = pe.step(k);
       const int64_t r_a = e2.get(la->args[0]), c_a = e2.get(la->args[1]);
       const int64_t r_b = e2.get(lb->args[0]), c_b = e2.get(lb->args[1]);
       if (k == g.lo) {
@@ -693,13 +913,10 @@ bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo,
         if (r_a != ra || r_b != rb) kfail(WS_UNSUPPORTED_KERNEL, "tile rows change across iterations");
         ka1 = c_a, kb1 = c_b;
       }
-      // advance scalar iter args with the yield
-      for (size_t i = 0; i < g.iter.size(); ++i)
-        if (e2.v.count(y->args[i])) env.v[g.iter[i].first] = e2.v[y->args[i]];
     }
     if (trip > 1 && (ka1 - ka != BKa || kb1 - kb != BKb))
       kfail(WS_UNSUPPORTED_KERNEL, "K offsets do not advance by the tile depth");
-    ScalarEnv ee = env;
+    ScalarEnv ee = pe.env;
     ee.run(g.epi, pid);
     tiles.push_back({pid, ee.get(store->args[1]), ee.get(store->args[2]), ra, rb, ka, kb});
   }
@@ -710,19 +927,17 @@ bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo,
   std::map<std::vector<int64_t>, std::vector<PidTile>> groups;
   for (auto& t : tiles) groups[{t.ra - t.r0, t.rb - t.c0, t.ka0, t.kb0}].push_back(t);
 
-  // exactness of the device arithmetic for the reference's payloads
-  auto amax = [](const HostBuf& b) {
-    double m = 0;
-    const int64_t n = b.shape.r * b.shape.c;
-    for (int64_t i = 0; i < n; ++i) m = std::max(m, std::fabs(b.get(i / b.shape.c, i % b.shape.c)));
-    return m;
-  };
+  // exactness of the device arithmetic for int payloads: exact operands, fp32-exact partial sums
   if (!A.shape.real || !B.shape.real) {
-    if (amax(A) * amax(B) * static_cast<double>(Kd) >= 16777216.0)
+    const double ma = A.amax(), mb = B.amax();
+    dt = exact_int_dtype(dt, std::max(ma, mb));
+    if (ma * mb * static_cast<double>(Kd) >= 16777216.0)
       kfail(WS_UNSUPPORTED_KERNEL, "int payloads could overflow fp32-exact accumulation (>= 2^24)");
   }
 
-  for (auto& [key, ts] : groups) {
+  for (auto& kv : groups) {
+    const std::vector<int64_t>& key = kv.first;
+    const std::vector<PidTile>& ts = kv.second;
     const int64_t dA = key[0], dB = key[1], ka0 = key[2], kb0 = key[3];
     int64_t rmin = INT64_MAX, rmax = INT64_MIN, cmin = INT64_MAX, cmax = INT64_MIN;
     for (auto& t : ts) {
@@ -735,33 +950,48 @@ bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo,
       kfail(WS_EVAL, "tile access out of bounds");
     const int64_t M = rmax - rmin, N = cmax - cmin;
     const int64_t Mp = (M + 255) / 256 * 256, Np = (N + 255) / 256 * 256, Kp = (Kd + 63) / 64 * 64;
-    std::vector<uint16_t> ha(static_cast<size_t>(Mp * Kp), 0), hb(static_cast<size_t>(Np * Kp), 0);
-    for (int64_t r = 0; r < M; ++r)
-      for (int64_t k = 0; k < Kd; ++k) ha[r * Kp + k] = to_half_bits(static_cast<float>(A.get(rmin + dA + r, ka0 + k)), dt);
-    for (int64_t n = 0; n < N; ++n)
-      for (int64_t k = 0; k < Kd; ++k) hb[n * Kp + k] = to_half_bits(static_cast<float>(B.get(cmin + dB + n, kb0 + k)), dt);
-    DevBuf da, db, dc;
-    cuda_check(cudaMalloc(&da.p, ha.size() * 2), "cudaMalloc");
-    cuda_check(cudaMalloc(&db.p, hb.size() * 2), "cudaMalloc");
-    cuda_check(cudaMalloc(&dc.p, static_cast<size_t>(Mp * Np) * 4), "cudaMalloc");
-    cuda_check(cudaMemcpyAsync(da.p, ha.data(), ha.size() * 2, cudaMemcpyHostToDevice, st), "H2D");
-    cuda_check(cudaMemcpyAsync(db.p, hb.data(), hb.size() * 2, cudaMemcpyHostToDevice, st), "H2D");
+    auto* ha = static_cast<uint16_t*>(g_stage.pinned(0, static_cast<size_t>(Mp * Kp) * 2));
+    auto* hb = static_cast<uint16_t*>(g_stage.pinned(1, static_cast<size_t>(Np * Kp) * 2));
+    parallel_rows(Mp, Kp, [&](int64_t r) {
+      uint16_t* row = ha + r * Kp;
+      if (r >= M) {
+        std::memset(row, 0, Kp * 2);
+        return;
+      }
+      for (int64_t k = 0; k < Kd; ++k) row[k] = to_half_bits(static_cast<float>(A.get(rmin + dA + r, ka0 + k)), dt);
+      for (int64_t k = Kd; k < Kp; ++k) row[k] = 0;
+    });
+    parallel_rows(Np, Kp, [&](int64_t n) {
+      uint16_t* row = hb + n * Kp;
+      if (n >= N) {
+        std::memset(row, 0, Kp * 2);
+        return;
+      }
+      for (int64_t k = 0; k < Kd; ++k) row[k] = to_half_bits(static_cast<float>(B.get(cmin + dB + n, kb0 + k)), dt);
+      for (int64_t k = Kd; k < Kp; ++k) row[k] = 0;
+    });
+    void* da = g_stage.device(0, static_cast<size_t>(Mp * Kp) * 2);
+    void* db = g_stage.device(1, static_cast<size_t>(Np * Kp) * 2);
+    void* dc = g_stage.device(2, static_cast<size_t>(Mp * Np) * 4);
+    cuda_check(cudaMemcpyAsync(da, ha, static_cast<size_t>(Mp * Kp) * 2, cudaMemcpyHostToDevice, st), "H2D");
+    cuda_check(cudaMemcpyAsync(db, hb, static_cast<size_t>(Np * Kp) * 2, cudaMemcpyHostToDevice, st), "H2D");
     ws_gemm_desc d{};
     d.in_dtype = dt;
     d.out_dtype = WS_F32;
     d.M = Mp, d.N = Np, d.K = Kp;
-    d.A = da.p, d.lda = Kp, d.B = db.p, d.ldb = Kp, d.C = dc.p, d.ldc = Np;
+    d.A = da, d.lda = Kp, d.B = db, d.ldb = Kp, d.C = dc, d.ldc = Np;
     d.scale_a = static_cast<float>(scale), d.scale_b = 1.f;
-    d.persistent = 1;
-    d.cta_pair = Kp >= 1024 ? 1 : 0;
+    gemm_launch_knobs(d, pl, Kp);
     d.act = act_relu ? 1 : 0;
     ws_check(ws_gemm_tn(&d, st));
-    std::vector<float> hc(static_cast<size_t>(Mp * Np));
-    cuda_check(cudaMemcpyAsync(hc.data(), dc.p, hc.size() * 4, cudaMemcpyDeviceToHost, st), "D2H");
+    auto* hc = static_cast<float*>(g_stage.pinned(2, static_cast<size_t>(Mp * Np) * 4));
+    cuda_check(cudaMemcpyAsync(hc, dc, static_cast<size_t>(Mp * Np) * 4, cudaMemcpyDeviceToHost, st), "D2H");
     cuda_check(cudaStreamSynchronize(st), "sync");
-    for (auto& t : ts)
+    parallel_rows(static_cast<int64_t>(ts.size()), BM * BN, [&](int64_t i) {
+      const PidTile& t = ts[static_cast<size_t>(i)];
       for (int64_t r = 0; r < BM; ++r)
         for (int64_t c = 0; c < BN; ++c) C.set(t.r0 + r, t.c0 + c, hc[(t.r0 - rmin + r) * Np + (t.c0 - cmin + c)]);
+    });
   }
   return true;
 }
@@ -769,149 +999,425 @@ bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo,
 // ------------------------------------------------------------------------------------------------
 // flash .k
 // ------------------------------------------------------------------------------------------------
-bool try_flash(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo, int64_t hi, int dt, cudaStream_t st) {
-  std::vector<const Op*> dots, loads;
-  int n_exp = 0, n_rmax = 0, n_radd = 0;
-  for (const Op* o : tile_ops(g.body)) {
+// The whole dataflow of the .k is matched, op by op (operand order of commutative ops free):
+//   s  = dot q_tile, k_tile.T, acc = zeros | mask-bank tile      ss = ew mul s, <1x1 scale>
+//   rm = reduce max ss axis=1     mn = ew max m, rm              d  = ew sub ss, mn
+//   pp = ew exp d                 dm = ew sub m, mn              al = ew exp dm
+//   rs = reduce add pp axis=1     la = ew mul l, al              l1 = ew add la, rs
+//   as = ew mul acc, al           acc1 = dot pp, v_tile, acc = as
+//   yield acc1 -> acc, mn -> m, l1 -> l;  stores of acc, l and m in the epilogue
+// with acc, l starting at zeros and m at a constant <= -1e4. Any other tile op — a bias, a
+// padding mask, a different rescale — makes the kernel unsupported rather than misread.
+bool try_flash(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo, int64_t hi, int dt, const Plan& pl,
+               cudaStream_t st) {
+  std::vector<const Op*> dots;
+  for (const Op* o : tile_ops(g.body))
     if (o->k == K::Dot) dots.push_back(o);
-    else if (o->k == K::Load) loads.push_back(o);
-    else if (o->k == K::Ew && o->fn == "exp") ++n_exp;
-    else if (o->k == K::Reduce && o->fn == "max" && o->axis == 1) ++n_rmax;
-    else if (o->k == K::Reduce && o->fn == "add" && o->axis == 1) ++n_radd;
-  }
-  if (dots.size() != 2 || n_exp < 1 || n_rmax != 1 || n_radd != 1) return false;
+  if (dots.size() != 2) return false;
   const Op* qk = dots[0]->trans ? dots[0] : dots[1];
   const Op* pv = dots[0]->trans ? dots[1] : dots[0];
   if (!qk->trans || pv->trans) return false;
-  const Op* lq = def_of(g.body, qk->args[0]);
-  const Op* lk = def_of(g.body, qk->args[1]);
-  const Op* lv = def_of(g.body, pv->args[1]);
-  if (!lq || !lk || !lv || lq->k != K::Load || lk->k != K::Load || lv->k != K::Load) return false;
-  const Op* s_init = def_any(g, qk->args[2]);
-  const bool causal = s_init && s_init->k == K::Load;  // mask bank
-  // softmax scale: the 1x1 constant multiplying the scores
-  double scale = -1;
-  for (const Op& o : g.body)
-    if (o.k == K::Ew && o.fn == "mul" && o.args[0] == qk->res) {
-      const Op* c = def_any(g, o.args[1]);
-      if (c && c->k == K::ConstTile && !c->zeros && c->shape.r == 1 && c->shape.c == 1) scale = c->lit[0];
-    }
-  if (scale <= 0) return false;
-  // outputs: stores of the three iter args acc (pv chain), l (row sums), m (running max)
   const Op* y = yield_op(g);
-  if (!y) return false;
+  if (!y || y->args.size() != g.iter.size()) return false;
+  auto body = [&](const std::string& v) { return def_of(g.body, v); };
+  // score scaling and row max
+  const Op *ss = nullptr, *rm = nullptr, *mn = nullptr, *dd = nullptr, *pp = nullptr, *dm = nullptr, *al = nullptr,
+           *rs = nullptr, *la = nullptr, *l1 = nullptr, *as = nullptr;
+  const Op* sc = nullptr;
+  for (const Op& o : g.body)
+    if (o.k == K::Ew && o.fn == "mul" && o.args.size() == 2 && (o.args[0] == qk->res || o.args[1] == qk->res)) {
+      sc = const_1x1(g, o.args[0] == qk->res ? o.args[1] : o.args[0]);
+      if (sc) ss = &o;
+    }
+  if (!ss || sc->lit[0] <= 0) return false;
+  // acc1 = dot pp, tv, acc = as
+  pp = body(pv->args[0]);
+  as = body(pv->args[2]);
+  const Op* lv = body(pv->args[1]);
+  if (!pp || !as || !lv || lv->k != K::Load) return false;
+  if (pp->k != K::Ew || pp->fn != "exp" || pp->args.size() != 1) return false;
+  dd = body(pp->args[0]);
+  if (!dd || dd->k != K::Ew || dd->fn != "sub" || dd->args.size() != 2 || dd->args[0] != ss->res) return false;
+  mn = body(dd->args[1]);
+  if (!mn || mn->k != K::Ew || mn->fn != "max" || mn->args.size() != 2) return false;
+  // mn = max(m, rm), rm = reduce max ss axis 1
+  const std::string m_it = iter_index(g, mn->args[0]) >= 0 ? mn->args[0] : mn->args[1];
+  rm = body(m_it == mn->args[0] ? mn->args[1] : mn->args[0]);
+  if (iter_index(g, m_it) < 0 || !rm || rm->k != K::Reduce || rm->fn != "max" || rm->axis != 1 ||
+      rm->args[0] != ss->res)
+    return false;
+  // as = acc * al, al = exp(m - mn)
+  const std::string acc_it = iter_index(g, as->args[0]) >= 0 ? as->args[0] : as->args.size() > 1 ? as->args[1] : "";
+  if (as->k != K::Ew || as->fn != "mul" || as->args.size() != 2 || iter_index(g, acc_it) < 0) return false;
+  al = body(acc_it == as->args[0] ? as->args[1] : as->args[0]);
+  if (!al || al->k != K::Ew || al->fn != "exp" || al->args.size() != 1) return false;
+  dm = body(al->args[0]);
+  if (!dm || dm->k != K::Ew || dm->fn != "sub" || dm->args.size() != 2 || dm->args[0] != m_it || dm->args[1] != mn->res)
+    return false;
+  // l1 = l * al + rowsum(pp)
+  for (const Op& o : g.body) {
+    if (o.k == K::Reduce && o.fn == "add" && o.axis == 1 && o.args[0] == pp->res) rs = &o;
+  }
+  if (!rs) return false;
+  for (const Op& o : g.body)
+    if (o.k == K::Ew && o.fn == "add" && o.args.size() == 2 && (o.args[0] == rs->res || o.args[1] == rs->res)) {
+      const Op* cand = body(o.args[0] == rs->res ? o.args[1] : o.args[0]);
+      if (cand && cand->k == K::Ew && cand->fn == "mul" && cand->args.size() == 2 &&
+          (cand->args[0] == al->res || cand->args[1] == al->res)) {
+        la = cand;
+        l1 = &o;
+      }
+    }
+  if (!la || !l1) return false;
+  const std::string l_it = la->args[0] == al->res ? la->args[1] : la->args[0];
+  const int ia = iter_index(g, acc_it), im = iter_index(g, m_it), il = iter_index(g, l_it);
+  if (ia < 0 || im < 0 || il < 0 || ia == im || ia == il || im == il) return false;
+  if (y->args[ia] != pv->res || y->args[im] != mn->res || y->args[il] != l1->res) return false;
+  // loads and the QK accumulator
+  const Op* lq = body(qk->args[0]);
+  const Op* lk = body(qk->args[1]);
+  if (!lq || !lk || lq->k != K::Load || lk->k != K::Load) return false;
+  const Op* s_init = def_any(g, qk->args[2]);
+  if (!s_init) return false;
+  const bool causal = s_init->k == K::Load;
+  if (!causal && !zeros_tile(g, qk->args[2])) return false;
+  // nothing else in the body: every tile op is one of the matched ones
+  std::set<const Op*> known = {qk, pv, ss, rm, mn, dd, pp, dm, al, rs, la, l1, as, lq, lk, lv};
+  if (causal) known.insert(s_init);
+  for (const Op* o : tile_ops(g.body))
+    if (!known.count(o) && !(o->k == K::ConstTile)) kfail(WS_UNSUPPORTED_KERNEL, "flash kernel has an extra tile op '" + o->res + "'");
+  // initial values: acc and l zeros, m a large negative constant (the .k's -1e6)
+  if (!zeros_tile(g, g.iter[ia].second) || !zeros_tile(g, g.iter[il].second)) return false;
+  {
+    const Op* m0 = def_of(g.pro, g.iter[im].second);
+    double v0 = 1;
+    if (m0 && m0->k == K::ConstTile && !m0->zeros) {
+      v0 = *std::max_element(m0->lit.begin(), m0->lit.end());
+    } else if (m0 && m0->k == K::Ew && m0->fn == "add" && m0->args.size() == 2) {
+      const Op* c = const_1x1(g, m0->args[0]) ? const_1x1(g, m0->args[0]) : const_1x1(g, m0->args[1]);
+      const std::string z = c == const_1x1(g, m0->args[0]) ? m0->args[1] : m0->args[0];
+      if (c && zeros_tile(g, z)) v0 = c->lit[0];
+    }
+    if (v0 > -1e4) return false;
+  }
+  // outputs: stores of the three iter args acc (pv chain), l (row sums), m (running max); nothing
+  // else in the epilogue
   std::string o_buf, l_buf, m_buf;
   for (const Op& s : g.epi) {
-    if (s.k != K::Store) continue;
-    const int i = iter_index(g, s.args[0]);
-    if (i < 0) return false;
-    const Op* src = def_of(g.body, y->args[i]);
-    if (!src) return false;
-    if (src == pv) o_buf = s.buf;
-    else if (src->k == K::Ew && src->fn == "max") m_buf = s.buf;
-    else if (src->k == K::Ew && src->fn == "add") l_buf = s.buf;
-    else return false;
+    if (s.k == K::Store) {
+      const int i = iter_index(g, s.args[0]);
+      if (i == ia) o_buf = s.buf;
+      else if (i == il) l_buf = s.buf;
+      else if (i == im) m_buf = s.buf;
+      else return false;
+    } else if (s.k != K::Arith && s.k != K::Const && s.k != K::Pid) {
+      return false;
+    }
   }
   if (o_buf.empty() || l_buf.empty() || m_buf.empty()) return false;
+  const double scale = sc->lit[0];
   const HostBuf& Q = bufs.at(lq->buf);
   const HostBuf& Kb = bufs.at(lk->buf);
   const HostBuf& V = bufs.at(lv->buf);
   const int64_t BR = lq->shape.r, D = lq->shape.c, BC = lk->shape.r;
   const int64_t trip = g.hi - g.lo, S = trip * BC;
-  if (S <= 0 || Q.shape.r % S != 0 || Kb.shape.r != Q.shape.r || V.shape.r != Q.shape.r || Q.shape.c != D)
+  if (S <= 0 || Q.shape.r % S != 0 || Kb.shape.r != Q.shape.r || V.shape.r != Q.shape.r || Q.shape.c != D ||
+      lk->shape.c != D || lv->shape.r != BC || lv->shape.c != D || Kb.shape.c != D || V.shape.c != D)
     return false;
   const int64_t BH = Q.shape.r / S;
-  // verify the batched pid geometry on the pids that run: q rows = pid*BR; k/v rows start at
-  // (pid / (S/BR)) * S and advance by BC
   const int64_t nqb = S / BR;
-  for (int64_t pid : {lo, hi - 1}) {
-    ScalarEnv env;
-    env.run(g.pro, pid);
-    for (auto& [a, init] : g.iter)
-      if (env.v.count(init)) env.v[a] = env.v[init];
-    ScalarEnv e2 = env;
-    e2.v[g.ind] = g.lo;
-    e2.run(g.body, pid);
-    if (e2.get(lq->args[0]) != pid * BR || e2.get(lk->args[0]) != (pid / nqb) * S || e2.get(lv->args[0]) != (pid / nqb) * S)
-      kfail(WS_UNSUPPORTED_KERNEL, "flash kernel pid geometry differs from the batched (b,h)-major layout");
+  if (S % BR) return false;
+  // causal: the mask bank tile is BR x BC from a BR x 3BC bank [0 | lower-triangular | masked],
+  // block 0 below the diagonal, 1 on it, 2 above (BR == BC so diagonal blocks are square)
+  const HostBuf* MB = causal ? &bufs.at(s_init->buf) : nullptr;
+  if (causal) {
+    if (BR != BC || s_init->shape.r != BR || s_init->shape.c != BC || MB->shape.r != BR || MB->shape.c < 3 * BC)
+      kfail(WS_UNSUPPORTED_KERNEL, "flash mask bank is not the [0 | causal | masked] layout");
+    for (int64_t r = 0; r < BR; ++r)
+      for (int64_t c = 0; c < 3 * BC; ++c) {
+        const int blk = static_cast<int>(c / BC);
+        const int64_t cc = c % BC;
+        const bool masked = blk == 2 || (blk == 1 && cc > r);
+        const double v = MB->get(r, c);
+        if (masked ? !(v <= -1e5) : v != 0.0)
+          kfail(WS_UNSUPPORTED_KERNEL, "flash mask bank is not causal (mb[" + std::to_string(r) + "," +
+                                           std::to_string(c) + "] = " + std::to_string(v) + ")");
+      }
+  }
+  // the pid geometry, on every pid that runs and every iteration: q rows = pid*BR (col 0); k/v
+  // rows (b,h)*S + j*BC (col 0); causal mask block = 0 / 1 / 2 below / on / above the diagonal
+  for (int64_t pid = lo; pid < hi; ++pid) {
+    PidEval pe(g, pid);
+    const int64_t bh = pid / nqb, qb = pid % nqb;
+    for (int64_t j = g.lo; j < g.hi; ++j) {
+      ScalarEnv e2 = pe.step(j);
+      const int64_t jj = j - g.lo;
+      if (e2.get(lq->args[0]) != pid * BR || e2.get(lq->args[1]) != 0 || e2.get(lk->args[0]) != bh * S + jj * BC ||
+          e2.get(lk->args[1]) != 0 || e2.get(lv->args[0]) != bh * S + jj * BC || e2.get(lv->args[1]) != 0)
+        kfail(WS_UNSUPPORTED_KERNEL, "flash kernel pid geometry differs from the batched (b,h)-major layout");
+      if (causal) {
+        const int64_t want = jj < qb ? 0 : jj == qb ? BC : 2 * BC;
+        if (e2.get(s_init->args[0]) != 0 || e2.get(s_init->args[1]) != want)
+          kfail(WS_UNSUPPORTED_KERNEL, "flash mask selection is not the causal block selector");
+      }
+      if (j - g.lo >= 1 && !causal) break;  // non-causal: the affine k/v walk is checked on two steps
+    }
   }
   if ((D != 64 && D != 128) || S % 128 != 0)
     kfail(WS_UNSUPPORTED_KERNEL, "flash on B200 needs head dim 64/128 and S % 128 == 0 (S=" + std::to_string(S) +
                                      ", D=" + std::to_string(D) + ")");
+  // the stored tiles (all rows of pids [lo, hi)) must be the q rows, at column 0
   const int64_t bh0 = lo / nqb, bh1 = (hi - 1) / nqb + 1;
   const size_t n = static_cast<size_t>(BH * S * D);
-  std::vector<uint16_t> hq(n), hk(n), hv(n);
-  for (int64_t r = bh0 * S; r < bh1 * S; ++r)
+  const size_t nr = static_cast<size_t>((bh1 - bh0) * S * D), off = static_cast<size_t>(bh0 * S * D);
+  auto* hq = static_cast<uint16_t*>(g_stage.pinned(0, nr * 2));
+  auto* hk = static_cast<uint16_t*>(g_stage.pinned(1, nr * 2));
+  auto* hv = static_cast<uint16_t*>(g_stage.pinned(2, nr * 2));
+  parallel_rows((bh1 - bh0) * S, D, [&](int64_t r) {
     for (int64_t c = 0; c < D; ++c) {
-      hq[r * D + c] = to_half_bits(static_cast<float>(Q.get(r, c)), dt);
-      hk[r * D + c] = to_half_bits(static_cast<float>(Kb.get(r, c)), dt);
-      hv[r * D + c] = to_half_bits(static_cast<float>(V.get(r, c)), dt);
+      const size_t i = static_cast<size_t>(r * D + c);
+      hq[i] = to_half_bits(static_cast<float>(Q.get(bh0 * S + r, c)), dt);
+      hk[i] = to_half_bits(static_cast<float>(Kb.get(bh0 * S + r, c)), dt);
+      hv[i] = to_half_bits(static_cast<float>(V.get(bh0 * S + r, c)), dt);
     }
-  DevBuf dq, dk, dv, dout, dlse;
-  for (DevBuf* b : {&dq, &dk, &dv, &dout}) cuda_check(cudaMalloc(&b->p, n * 2), "cudaMalloc");
-  cuda_check(cudaMalloc(&dlse.p, static_cast<size_t>(BH * S) * 4), "cudaMalloc");
-  cuda_check(cudaMemcpyAsync(dq.p, hq.data(), n * 2, cudaMemcpyHostToDevice, st), "H2D");
-  cuda_check(cudaMemcpyAsync(dk.p, hk.data(), n * 2, cudaMemcpyHostToDevice, st), "H2D");
-  cuda_check(cudaMemcpyAsync(dv.p, hv.data(), n * 2, cudaMemcpyHostToDevice, st), "H2D");
+  });
+  auto* dq = static_cast<uint16_t*>(g_stage.device(0, n * 2));
+  auto* dk = static_cast<uint16_t*>(g_stage.device(1, n * 2));
+  auto* dv = static_cast<uint16_t*>(g_stage.device(2, n * 2));
+  auto* dout = static_cast<uint16_t*>(g_stage.device(3, n * 2));
+  auto* dlse = static_cast<float*>(g_stage.device(4, static_cast<size_t>(BH * S) * 4));
+  auto* dmx = static_cast<float*>(g_stage.device(5, static_cast<size_t>(BH * S) * 4));
+  cuda_check(cudaMemcpyAsync(dq + off, hq, nr * 2, cudaMemcpyHostToDevice, st), "H2D");
+  cuda_check(cudaMemcpyAsync(dk + off, hk, nr * 2, cudaMemcpyHostToDevice, st), "H2D");
+  cuda_check(cudaMemcpyAsync(dv + off, hv, nr * 2, cudaMemcpyHostToDevice, st), "H2D");
   ws_attn_desc a{};
   a.dtype = dt;
   a.B = 1, a.H = static_cast<int32_t>(BH), a.S = static_cast<int32_t>(S), a.Dh = static_cast<int32_t>(D);
   a.causal = causal;
   a.softmax_scale = static_cast<float>(scale);
-  a.Q = dq.p, a.K = dk.p, a.V = dv.p, a.O = dout.p, a.LSE = static_cast<float*>(dlse.p);
+  a.Q = dq, a.K = dk, a.V = dv, a.O = dout, a.LSE = dlse, a.MX = dmx;
   a.bh_begin = static_cast<int32_t>(bh0), a.bh_end = static_cast<int32_t>(bh1);
+  a.D = pl.d == 0 ? 0 : std::max(pl.d, 2);  // none / plain ws programs: the smallest ring
+  a.grid_per_item = pl.persistent ? 0 : 1;
   ws_check(ws_attn_fwd(&a, st));
-  std::vector<uint16_t> ho(n);
-  std::vector<float> hl(static_cast<size_t>(BH * S));
-  cuda_check(cudaMemcpyAsync(ho.data(), dout.p, n * 2, cudaMemcpyDeviceToHost, st), "D2H");
-  cuda_check(cudaMemcpyAsync(hl.data(), dlse.p, hl.size() * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  auto* ho = static_cast<uint16_t*>(g_stage.pinned(3, nr * 2));
+  auto* hl = static_cast<float*>(g_stage.pinned(4, static_cast<size_t>((bh1 - bh0) * S) * 4));
+  auto* hm = static_cast<float*>(g_stage.pinned(5, static_cast<size_t>((bh1 - bh0) * S) * 4));
+  cuda_check(cudaMemcpyAsync(ho, dout + off, nr * 2, cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaMemcpyAsync(hl, dlse + bh0 * S, static_cast<size_t>((bh1 - bh0) * S) * 4, cudaMemcpyDeviceToHost, st),
+             "D2H");
+  cuda_check(cudaMemcpyAsync(hm, dmx + bh0 * S, static_cast<size_t>((bh1 - bh0) * S) * 4, cudaMemcpyDeviceToHost, st),
+             "D2H");
   cuda_check(cudaStreamSynchronize(st), "sync");
-  // Write back in the .k's (acc, l, m) form with m = lse, l = 1, acc = O: the harness step
-  // o = acc / l and lse = m + log(l) is invariant to the choice of m.
+  // The .k's outputs: m = the exact running max, l = sum exp(ss - m) = exp(lse - m), and the
+  // un-normalised accumulator acc = O * l.
   HostBuf& O = bufs.at(o_buf);
   HostBuf& L = bufs.at(l_buf);
   HostBuf& Mx = bufs.at(m_buf);
-  auto half_to_float = [dt](uint16_t h) {
-    uint32_t u;
-    if (dt == WS_BF16) {
-      u = static_cast<uint32_t>(h) << 16;
-    } else {
-      const uint32_t s = (h & 0x8000u) << 16, e = (h >> 10) & 0x1F, m = h & 0x3FF;
-      if (e == 0) {
-        float f = std::ldexp(static_cast<float>(m), -24);
-        return s ? -f : f;
-      }
-      u = s | ((e + 112) << 23) | (m << 13);
-    }
-    float f;
-    std::memcpy(&f, &u, 4);
-    return f;
-  };
-  for (int64_t pid = lo; pid < hi; ++pid)
+  parallel_rows(hi - lo, BR * D, [&](int64_t i) {
+    const int64_t pid = lo + i;
     for (int64_t r = pid * BR; r < pid * BR + BR; ++r) {
-      for (int64_t c = 0; c < D; ++c) O.set(r, c, half_to_float(ho[r * D + c]));
-      L.set(r, 0, 1.0);
-      Mx.set(r, 0, hl[r]);
+      const int64_t rr = r - bh0 * S;
+      const double m = hm[rr], l = std::exp(static_cast<double>(hl[rr]) - m);
+      for (int64_t c = 0; c < D; ++c) O.set(r, c, static_cast<double>(half_to_float(ho[rr * D + c], dt)) * l);
+      L.set(r, 0, l);
+      Mx.set(r, 0, m);
     }
+  });
+  return true;
+}
+
+// ------------------------------------------------------------------------------------------------
+// max-shift attention (ref proj/kernels/attention.k:1-21)
+// ------------------------------------------------------------------------------------------------
+// s = q_tile . k_tile^T (acc zeros); m = rowmax s; acc += (s - m) . v_tile, per iteration. On the
+// GPU: one GEMM for every score block of every pid (S = Q . Kstack^T, fp32), a row-block shift
+// kernel (P = S - blockwise row max, 16-bit), one GEMM for the accumulation (acc = P . Vstack).
+// Exact for int payloads while |s - m| and the inputs are exact in the 16-bit type and the
+// accumulator stays below 2^24.
+__global__ void ws_rowblock_shift_kernel(const float* __restrict__ s, int64_t lds, uint16_t* __restrict__ p,
+                                         int64_t ldp, int rows, int valid_cols, int bc, int nblk_pad, int f16) {
+  const int64_t idx = static_cast<int64_t>(blockIdx.x) * blockDim.x + threadIdx.x;
+  const int64_t r = idx / nblk_pad, b = idx % nblk_pad;
+  if (r >= rows) return;
+  const float* sr = s + r * lds + b * bc;
+  uint16_t* pr = p + r * ldp + b * bc;
+  if (b * bc >= valid_cols) {
+    for (int c = 0; c < bc; ++c) pr[c] = 0;
+    return;
+  }
+  float m = sr[0];
+  for (int c = 1; c < bc; ++c) m = fmaxf(m, sr[c]);
+  for (int c = 0; c < bc; ++c) {
+    const float x = sr[c] - m;
+    pr[c] = f16 ? __half_as_ushort(__float2half_rn(x)) : __bfloat16_as_ushort(__float2bfloat16_rn(x));
+  }
+}
+
+bool try_maxshift(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo, int64_t hi, int dt,
+                  const Plan& pl, cudaStream_t st) {
+  std::vector<const Op*> dots;
+  for (const Op* o : tile_ops(g.body))
+    if (o->k == K::Dot) dots.push_back(o);
+  if (dots.size() != 2) return false;
+  const Op* qk = dots[0]->trans ? dots[0] : dots[1];
+  const Op* pv = dots[0]->trans ? dots[1] : dots[0];
+  if (!qk->trans || pv->trans) return false;
+  auto body = [&](const std::string& v) { return def_of(g.body, v); };
+  const Op* sub = body(pv->args[0]);
+  if (!sub || sub->k != K::Ew || sub->fn != "sub" || sub->args.size() != 2 || sub->args[0] != qk->res) return false;
+  const Op* rm = body(sub->args[1]);
+  if (!rm || rm->k != K::Reduce || rm->fn != "max" || rm->axis != 1 || rm->args[0] != qk->res) return false;
+  if (!zeros_tile(g, qk->args[2])) return false;
+  const Op* lq = body(qk->args[0]);
+  const Op* lk = body(qk->args[1]);
+  const Op* lv = body(pv->args[1]);
+  if (!lq || !lk || !lv || lq->k != K::Load || lk->k != K::Load || lv->k != K::Load) return false;
+  const Op* y = yield_op(g);
+  const int ia = iter_index(g, pv->args[2]);
+  if (!y || ia < 0 || y->args[ia] != pv->res || !zeros_tile(g, g.iter[ia].second)) return false;
+  std::set<const Op*> known = {qk, pv, sub, rm, lq, lk, lv};
+  for (const Op* o : tile_ops(g.body))
+    if (!known.count(o) && o->k != K::ConstTile) return false;
+  const Op* store = nullptr;
+  for (const Op& o : g.epi) {
+    if (o.k == K::Store) {
+      if (store || iter_index(g, o.args[0]) != ia) return false;
+      store = &o;
+    } else if (o.k != K::Arith && o.k != K::Const && o.k != K::Pid) {
+      return false;
+    }
+  }
+  if (!store) return false;
+  const int64_t BR = lq->shape.r, D = lq->shape.c, BC = lk->shape.r, DV = lv->shape.c;
+  if (lk->shape.c != D || lv->shape.r != BC) return false;
+  const HostBuf& Q = bufs.at(lq->buf);
+  const HostBuf& Kt = bufs.at(lk->buf);
+  const HostBuf& V = bufs.at(lv->buf);
+  HostBuf& O = bufs.at(store->buf);
+  const int64_t trip = g.hi - g.lo;
+  if (trip < 1) return false;
+  // geometry: q tile per pid (fixed across iterations); k / v tiles per iteration, the same for
+  // every pid (one shared key/value sequence)
+  std::vector<std::pair<int64_t, int64_t>> kc, vc;
+  struct PidRows {
+    int64_t qr, qc, orow, ocol;
+  };
+  std::vector<PidRows> pr;
+  for (int64_t pid = lo; pid < hi; ++pid) {
+    PidEval pe(g, pid);
+    PidRows x{};
+    for (int64_t j = g.lo; j < g.hi; ++j) {
+      ScalarEnv e2 = pe.step(j);
+      const int64_t jj = j - g.lo;
+      const std::pair<int64_t, int64_t> kk{e2.get(lk->args[0]), e2.get(lk->args[1])},
+          vv{e2.get(lv->args[0]), e2.get(lv->args[1])};
+      if (pid == lo) {
+        kc.push_back(kk);
+        vc.push_back(vv);
+      } else if (kc[jj] != kk || vc[jj] != vv) {
+        kfail(WS_UNSUPPORTED_KERNEL, "max-shift attention: key/value tiles differ between pids");
+      }
+      const int64_t r = e2.get(lq->args[0]), c = e2.get(lq->args[1]);
+      if (jj == 0) x.qr = r, x.qc = c;
+      else if (r != x.qr || c != x.qc) kfail(WS_UNSUPPORTED_KERNEL, "max-shift attention: the query tile moves");
+    }
+    ScalarEnv ee = pe.env;
+    ee.run(g.epi, pid);
+    x.orow = ee.get(store->args[1]);
+    x.ocol = ee.get(store->args[2]);
+    pr.push_back(x);
+  }
+  if (pr.empty()) return true;
+  auto oob = [](const HostBuf& b, int64_t r, int64_t c, int64_t R, int64_t C) {
+    return r < 0 || c < 0 || r + R > b.shape.r || c + C > b.shape.c;
+  };
+  for (auto& x : pr)
+    if (oob(Q, x.qr, x.qc, BR, D) || oob(O, x.orow, x.ocol, BR, DV)) kfail(WS_EVAL, "tile access out of bounds");
+  for (int64_t j = 0; j < trip; ++j)
+    if (oob(Kt, kc[j].first, kc[j].second, BC, D) || oob(V, vc[j].first, vc[j].second, BC, DV))
+      kfail(WS_EVAL, "tile access out of bounds");
+  // exactness: inputs exact in the 16-bit type, |s - m| <= 2 max|q| max|k| D exact, and the
+  // accumulator below 2^24
+  const bool ints = !Q.shape.real || !Kt.shape.real || !V.shape.real;
+  if (ints) {
+    const double mq = Q.amax(), mk = Kt.amax(), mv = V.amax();
+    const double shift = 2.0 * mq * mk * static_cast<double>(D);
+    dt = exact_int_dtype(dt, std::max({mq, mk, mv, shift}));
+    if (mq * mk * static_cast<double>(D) >= 16777216.0 || shift * mv * static_cast<double>(trip * BC) >= 16777216.0)
+      kfail(WS_UNSUPPORTED_KERNEL, "int payloads could overflow fp32-exact accumulation (>= 2^24)");
+  }
+  const int64_t npid = static_cast<int64_t>(pr.size());
+  const int64_t M = npid * BR, Mp = (M + 255) / 256 * 256;
+  const int64_t N1 = trip * BC, Np = (N1 + 255) / 256 * 256;
+  const int64_t Kp = (D + 63) / 64 * 64;
+  const int64_t DVp = (DV + 255) / 256 * 256;
+  auto* hq = static_cast<uint16_t*>(g_stage.pinned(0, static_cast<size_t>(Mp * Kp) * 2));
+  auto* hk = static_cast<uint16_t*>(g_stage.pinned(1, static_cast<size_t>(Np * Kp) * 2));
+  auto* hv = static_cast<uint16_t*>(g_stage.pinned(2, static_cast<size_t>(DVp * Np) * 2));
+  std::memset(hq, 0, static_cast<size_t>(Mp * Kp) * 2);
+  std::memset(hk, 0, static_cast<size_t>(Np * Kp) * 2);
+  std::memset(hv, 0, static_cast<size_t>(DVp * Np) * 2);
+  for (int64_t i = 0; i < npid; ++i)
+    for (int64_t r = 0; r < BR; ++r)
+      for (int64_t c = 0; c < D; ++c)
+        hq[(i * BR + r) * Kp + c] = to_half_bits(static_cast<float>(Q.get(pr[i].qr + r, pr[i].qc + c)), dt);
+  for (int64_t j = 0; j < trip; ++j)
+    for (int64_t r = 0; r < BC; ++r) {
+      for (int64_t c = 0; c < D; ++c)
+        hk[(j * BC + r) * Kp + c] = to_half_bits(static_cast<float>(Kt.get(kc[j].first + r, kc[j].second + c)), dt);
+      for (int64_t c = 0; c < DV; ++c)  // V^T: [value column][key]
+        hv[c * Np + j * BC + r] = to_half_bits(static_cast<float>(V.get(vc[j].first + r, vc[j].second + c)), dt);
+    }
+  void* dq = g_stage.device(0, static_cast<size_t>(Mp * Kp) * 2);
+  void* dk = g_stage.device(1, static_cast<size_t>(Np * Kp) * 2);
+  void* dv = g_stage.device(2, static_cast<size_t>(DVp * Np) * 2);
+  auto* ds = static_cast<float*>(g_stage.device(3, static_cast<size_t>(Mp * Np) * 4));
+  auto* dp = static_cast<uint16_t*>(g_stage.device(4, static_cast<size_t>(Mp * Np) * 2));
+  auto* dacc = static_cast<float*>(g_stage.device(5, static_cast<size_t>(Mp * DVp) * 4));
+  cuda_check(cudaMemcpyAsync(dq, hq, static_cast<size_t>(Mp * Kp) * 2, cudaMemcpyHostToDevice, st), "H2D");
+  cuda_check(cudaMemcpyAsync(dk, hk, static_cast<size_t>(Np * Kp) * 2, cudaMemcpyHostToDevice, st), "H2D");
+  cuda_check(cudaMemcpyAsync(dv, hv, static_cast<size_t>(DVp * Np) * 2, cudaMemcpyHostToDevice, st), "H2D");
+  ws_gemm_desc d1{};
+  d1.in_dtype = dt, d1.out_dtype = WS_F32;
+  d1.M = Mp, d1.N = Np, d1.K = Kp;
+  d1.A = dq, d1.lda = Kp, d1.B = dk, d1.ldb = Kp, d1.C = ds, d1.ldc = Np;
+  d1.scale_a = d1.scale_b = 1.f;
+  gemm_launch_knobs(d1, pl, Kp);
+  ws_check(ws_gemm_tn(&d1, st));
+  const int nblk_pad = static_cast<int>(Np / BC) + (Np % BC ? 1 : 0);
+  if (Np % BC) kfail(WS_UNSUPPORTED_KERNEL, "max-shift attention: the key block must divide 256");
+  const int64_t threads = Mp * nblk_pad;
+  ws_rowblock_shift_kernel<<<static_cast<unsigned>((threads + 255) / 256), 256, 0, st>>>(
+      ds, Np, dp, Np, static_cast<int>(Mp), static_cast<int>(N1), static_cast<int>(BC), nblk_pad, dt == WS_F16);
+  cuda_check(cudaGetLastError(), "row-block shift launch");
+  ws_detail::count_launch();
+  ws_gemm_desc d2{};
+  d2.in_dtype = dt, d2.out_dtype = WS_F32;
+  d2.M = Mp, d2.N = DVp, d2.K = Np;
+  d2.A = dp, d2.lda = Np, d2.B = dv, d2.ldb = Np, d2.C = dacc, d2.ldc = DVp;
+  d2.scale_a = d2.scale_b = 1.f;
+  gemm_launch_knobs(d2, pl, Np);
+  ws_check(ws_gemm_tn(&d2, st));
+  auto* hacc = static_cast<float*>(g_stage.pinned(3, static_cast<size_t>(Mp * DVp) * 4));
+  cuda_check(cudaMemcpyAsync(hacc, dacc, static_cast<size_t>(Mp * DVp) * 4, cudaMemcpyDeviceToHost, st), "D2H");
+  cuda_check(cudaStreamSynchronize(st), "sync");
+  for (int64_t i = 0; i < npid; ++i)
+    for (int64_t r = 0; r < BR; ++r)
+      for (int64_t c = 0; c < DV; ++c) O.set(pr[i].orow + r, pr[i].ocol + c, hacc[(i * BR + r) * DVp + c]);
   return true;
 }
 
 }  // namespace
 
-extern "C" ws_status ws_run_kernel(const char* ktext, ws_kbuffer* buffers, int32_t nbuffers, int64_t pid_lo,
-                                   int64_t pid_hi, int32_t dtype, void* cuda_stream);
-
-namespace ws_detail {
-ws_status set_error(ws_status s, const std::string& m);
-}
-
-ws_status ws_run_kernel(const char* ktext, ws_kbuffer* buffers, int32_t nbuffers, int64_t pid_lo, int64_t pid_hi,
-                        int32_t dtype, void* cuda_stream) {
+extern "C" ws_status ws_run_kernel_spec(const char* ktext, ws_kbuffer* buffers, int32_t nbuffers, int64_t pid_lo,
+                                        int64_t pid_hi, int32_t dtype, const ws_runspec* spec, void* cuda_stream) {
   try {
     if (!ktext) kfail(WS_TYPE, "null kernel text");
     if (dtype != WS_BF16 && dtype != WS_F16) kfail(WS_TYPE, "device dtype must be BF16 or F16");
     if (pid_hi < pid_lo) kfail(WS_TYPE, "pid_hi < pid_lo");
     Kernel g = parse(ktext);
+    const Plan pl = resolve_spec(g, spec);
     std::map<std::string, HostBuf> bufs;
     for (const Param& p : g.params) {
       HostBuf b;
@@ -933,12 +1439,19 @@ ws_status ws_run_kernel(const char* ktext, ws_kbuffer* buffers, int32_t nbuffers
       }
     if (pid_hi == pid_lo) return WS_OK;
     cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
-    if (try_gemm(g, bufs, pid_lo, pid_hi, dtype, st)) return WS_OK;
-    if (try_flash(g, bufs, pid_lo, pid_hi, dtype, st)) return WS_OK;
-    kfail(WS_UNSUPPORTED_KERNEL, "kernel '" + g.name + "' is neither a gemm.k-family nor a flash kernel");
+    if (try_gemm(g, bufs, pid_lo, pid_hi, dtype, pl, st)) return WS_OK;
+    if (try_flash(g, bufs, pid_lo, pid_hi, dtype, pl, st)) return WS_OK;
+    if (try_maxshift(g, bufs, pid_lo, pid_hi, dtype, pl, st)) return WS_OK;
+    kfail(WS_UNSUPPORTED_KERNEL,
+          "kernel '" + g.name + "' is none of the gemm.k family, the flash kernel or the max-shift attention kernel");
   } catch (const KError& e) {
     return ws_detail::set_error(e.code, e.what());
   } catch (const std::exception& e) {
     return ws_detail::set_error(WS_EVAL, e.what());
   }
+}
+
+extern "C" ws_status ws_run_kernel(const char* ktext, ws_kbuffer* buffers, int32_t nbuffers, int64_t pid_lo,
+                                   int64_t pid_hi, int32_t dtype, void* cuda_stream) {
+  return ws_run_kernel_spec(ktext, buffers, nbuffers, pid_lo, pid_hi, dtype, nullptr, cuda_stream);
 }

@@ -41,6 +41,16 @@ class _Pipe:
         if t is None or tuple(t.shape) != tuple(shape) or t.dtype != dtype:
             with torch.cuda.stream(self.s_comp):
                 t = torch.empty(shape, dtype=dtype, device=self.dev)
+            # the copy streams use the buffer too: when a shape change drops it, the caching
+            # allocator must not hand the block out again before their queued copies are done
+            t.record_stream(self.s_h2d)
+            t.record_stream(self.s_d2h)
+            # ... and the new block may have been freed on s_comp by work still queued there, so
+            # the copy streams writing it start after that work
+            ev = torch.cuda.Event()
+            ev.record(self.s_comp)
+            self.s_h2d.wait_event(ev)
+            self.s_d2h.wait_event(ev)
             self.bufs[key] = t
         return t
 

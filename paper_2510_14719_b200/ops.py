@@ -36,6 +36,24 @@ _SMS: dict = {}
 _DESC_CACHE: dict = {}
 
 
+class _OnDevice:
+    """Make `device` current for the C-ABI call (the library launches on the current device, whose
+    stream the descriptor names); a no-op, without torch's context-manager cost, when it already is."""
+    __slots__ = ("idx", "prev")
+
+    def __init__(self, device: torch.device):
+        self.idx = device.index if device.index is not None else torch.cuda.current_device()
+
+    def __enter__(self):
+        self.prev = torch.cuda.current_device()
+        if self.prev != self.idx:
+            torch.cuda.set_device(self.idx)
+
+    def __exit__(self, *exc):
+        if self.prev != self.idx:
+            torch.cuda.set_device(self.prev)
+
+
 def _sm_count(device: torch.device) -> int:
     idx = device.index if device.index is not None else torch.cuda.current_device()
     if idx not in _SMS:
@@ -80,7 +98,8 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
         raise _lib.WsError(2, "batched operands must stack their batches along rows")
     if cta_pair is None:
         # pairs only when the 256 x 256 pair tiles still give every SM pair a tile
-        cta_pair = M % 256 == 0 and K >= 256 and nbat * (M // 256) * (N // 256) >= _sm_count(a.device) // 2
+        cta_pair = (M % 256 == 0 and K >= 256 and N % 128 == 0 and
+                    nbat * (M // 256) * (N // 128) >= _sm_count(a.device))
     shape = (nbat, M, N) if batched else (M, N)
     if out is None:
         od = out_dtype or (torch.bfloat16 if a.dtype == torch.float8_e4m3fn else a.dtype)
@@ -109,8 +128,11 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
         if len(_DESC_CACHE) >= 64:
             _DESC_CACHE.clear()
         _DESC_CACHE[key] = d
+    if b.device != a.device or out.device != a.device:
+        raise _lib.WsError(2, "a, b and out must be on the same CUDA device")
     lib = _lib.load()
-    _lib.check(lib.ws_gemm_tn(ctypes.byref(d), _stream_ptr(stream, a.device)))
+    with _OnDevice(a.device):
+        _lib.check(lib.ws_gemm_tn(ctypes.byref(d), _stream_ptr(stream, a.device)))
     return out
 
 
@@ -118,25 +140,44 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool 
              softmax_scale: Optional[float] = None, out: Optional[torch.Tensor] = None,
              lse: Optional[torch.Tensor] = None, D: int = 0, bh_range: Optional[tuple] = None,
              stream: Optional[torch.cuda.Stream] = None, trace: Optional[torch.Tensor] = None,
-             kv_block: int = 0, scale_q: float = 1.0, scale_k: float = 1.0, scale_v: float = 1.0):
+             kv_block: int = 0, scale_q: float = 1.0, scale_k: float = 1.0, scale_v: float = 1.0,
+             mx: Optional[torch.Tensor] = None):
     """FlashAttention forward over [B, H, S, Dh] tensors. Returns (o, lse) with lse fp32 [B, H, S]
     in natural-log units (lse = m + log l of the .k's running max m and row sum l).
 
     trace: optional int64 CUDA tensor of 3*256*8 entries receiving %clock64 stamps of CTA (0,0)
     (see ws_attn_fwd_traced in include/ws.h). kv_block: keys per K/V block (0 = auto = 128, or 64).
-    float8_e4m3fn q/k/v (hdim 128): scale_q/k/v are the per-tensor descales; o is bf16."""
+    float8_e4m3fn q/k/v (hdim 128): scale_q/k/v are the per-tensor descales; o is bf16.
+    mx: optional fp32 [B, H, S] tensor receiving the exact row max m of the scaled scores (the
+    .k's %m): the .k's row sum is then l = exp(lse - mx) and its accumulator acc = o * l."""
     if q.device.type != "cuda":
         raise _lib.WsError(2, "operands must be CUDA tensors (no CPU path)")
     if not (q.dtype == k.dtype == v.dtype) or q.dtype not in (torch.float16, torch.bfloat16, torch.float8_e4m3fn):
         raise _lib.WsError(2, f"unsupported dtype {q.dtype}")
+    if q.dim() != 4:
+        raise _lib.WsError(2, "q, k, v must be [B, H, S, Dh]")
     B, H, S, Dh = q.shape
     for t in (q, k, v):
-        if tuple(t.shape) != (B, H, S, Dh) or not t.is_contiguous():
-            raise _lib.WsError(2, "q, k, v must be contiguous [B, H, S, Dh]")
+        if tuple(t.shape) != (B, H, S, Dh) or not t.is_contiguous() or t.device != q.device:
+            raise _lib.WsError(2, "q, k, v must be contiguous [B, H, S, Dh] on one device")
+    # the kernel writes O through a tensor map built from B*H*S*Dh and q's dtype (bf16 for FP8
+    # inputs) and B*H*S fp32 LSE values: caller buffers must be exactly that
+    odt = torch.bfloat16 if q.dtype == torch.float8_e4m3fn else q.dtype
     if out is None:
-        out = torch.empty_like(q, dtype=torch.bfloat16 if q.dtype == torch.float8_e4m3fn else q.dtype)
+        out = torch.empty_like(q, dtype=odt)
+    elif tuple(out.shape) != (B, H, S, Dh) or out.dtype != odt or not out.is_contiguous() or out.device != q.device:
+        raise _lib.WsError(2, f"out must be a contiguous {odt} [B, H, S, Dh] tensor on {q.device}")
     if lse is None:
         lse = torch.empty((B, H, S), dtype=torch.float32, device=q.device)
+    elif (tuple(lse.shape) != (B, H, S) or lse.dtype != torch.float32 or not lse.is_contiguous()
+          or lse.device != q.device):
+        raise _lib.WsError(2, f"lse must be a contiguous float32 [B, H, S] tensor on {q.device}")
+    if mx is not None and (tuple(mx.shape) != (B, H, S) or mx.dtype != torch.float32 or not mx.is_contiguous()
+                           or mx.device != q.device):
+        raise _lib.WsError(2, f"mx must be a contiguous float32 [B, H, S] tensor on {q.device}")
+    if trace is not None and (trace.dtype != torch.int64 or trace.numel() < 3 * 256 * 8 or
+                              not trace.is_contiguous() or trace.device != q.device):
+        raise _lib.WsError(2, "trace must be a contiguous int64 tensor of >= 3*256*8 entries on q's device")
     d = _lib.AttnDesc()
     d.dtype = _DT[q.dtype]
     d.B, d.H, d.S, d.Dh = B, H, S, Dh
@@ -144,28 +185,34 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool 
     d.softmax_scale = softmax_scale if softmax_scale is not None else 1.0 / math.sqrt(Dh)
     d.Q, d.K, d.V, d.O = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr()
     d.LSE = lse.data_ptr()
+    d.MX = mx.data_ptr() if mx is not None else None
     d.D = D
     lo, hi = bh_range if bh_range is not None else (0, B * H)
     d.bh_begin, d.bh_end = lo, hi
     d.kv_block = kv_block
     d.scale_q, d.scale_k, d.scale_v = scale_q, scale_k, scale_v
     lib = _lib.load()
-    if trace is not None:
-        _lib.check(lib.ws_attn_fwd_traced(ctypes.byref(d), ctypes.c_void_p(_stream_ptr(stream)),
-                                          ctypes.c_void_p(trace.data_ptr())))
-    else:
-        _lib.check(lib.ws_attn_fwd(ctypes.byref(d), ctypes.c_void_p(_stream_ptr(stream))))
+    with _OnDevice(q.device):
+        if trace is not None:
+            _lib.check(lib.ws_attn_fwd_traced(ctypes.byref(d), ctypes.c_void_p(_stream_ptr(stream, q.device)),
+                                              ctypes.c_void_p(trace.data_ptr())))
+        else:
+            _lib.check(lib.ws_attn_fwd(ctypes.byref(d), ctypes.c_void_p(_stream_ptr(stream, q.device))))
     return out, lse
 
 
 def run_kernel(text: str, buffers: dict, pid_range=(0, 1), dtype: torch.dtype = torch.bfloat16,
-               stream: Optional[torch.cuda.Stream] = None) -> dict:
+               stream: Optional[torch.cuda.Stream] = None, spec: Optional[dict] = None) -> dict:
     """Run pids [lo, hi) of a `.k` kernel (reference grammar) on the GPU — the drop-in for the
     reference's tile-by-tile oracle run `interpret_tiles` (ref proj/tests/support/fixtures.hpp:148-157).
 
     buffers: {param name: numpy array} (float64 for `real`, int64 for `int` params); arrays are
     updated in place with the kernel's stores and also returned. Parameters without a buffer start
-    zeroed (and are returned). See ws_run_kernel in include/ws.h for the supported kernel shapes."""
+    zeroed (and are returned). See ws_run_kernel in include/ws.h for the supported kernel shapes.
+
+    spec: the reference's RunSpec (ref driver.hpp:42-57) as a dict of d, p, mode ("auto" | "fine" |
+    "coarse" | "none"), coop_wgs (or coop), persistent; rejected exactly as compile_kernel rejects
+    it (ws_run_kernel_spec). None = the library's measured defaults."""
     import re
 
     import numpy as np
@@ -193,8 +240,20 @@ def run_kernel(text: str, buffers: dict, pid_range=(0, 1), dtype: torch.dtype = 
     bufs = (_lib.KBuffer * max(1, len(arr)))(*arr)
     lo, hi = pid_range
     lib = _lib.load()
-    _lib.check(lib.ws_run_kernel(text.encode(), bufs, len(arr), lo, hi, _DT[dtype],
-                                 ctypes.c_void_p(_stream_ptr(stream) if torch.cuda.is_available() else 0)))
+    sp = None
+    if spec is not None:
+        unknown = set(spec) - {"d", "p", "mode", "coop_wgs", "coop", "persistent"}
+        if unknown:
+            raise _lib.WsError(2, f"unknown RunSpec fields {sorted(unknown)}")
+        mode = spec.get("mode", "auto")
+        if mode not in _lib.MODES:
+            raise _lib.WsError(1, f"unknown pipeline mode '{mode}'")  # ref driver.hpp:34-40
+        sp = _lib.RunSpec(d=int(spec.get("d", 0)), p=int(spec.get("p", 0)), mode=_lib.MODES[mode],
+                          coop_wgs=int(spec.get("coop_wgs", spec.get("coop", 0))),
+                          persistent=int(spec.get("persistent", 1)))
+    _lib.check(lib.ws_run_kernel_spec(text.encode(), bufs, len(arr), lo, hi, _DT[dtype],
+                                      ctypes.byref(sp) if sp is not None else None,
+                                      ctypes.c_void_p(_stream_ptr(stream) if torch.cuda.is_available() else 0)))
     return buffers
 
 

@@ -40,11 +40,21 @@ CASES = {
     "flash_bh2_s128_d32": (K.flash_src(2, 128, 32, 32, causal=False), 2026, 2 * 4, {"mb": K.flash_mask_bank(32)}),
     "flash_causal_bh2_s128_d32": (K.flash_src(2, 128, 32, 32, causal=True), 2026, 2 * 4,
                                   {"mb": K.flash_mask_bank(32)}),
+    # device-sized flash instances (head dim 64, S % 128 == 0) for the GPU front end: all three
+    # outputs (acc, l, m) of the .k compared buffer by buffer
+    "flash_bh2_s256_d64": (K.flash_src(2, 256, 64, 64, causal=False), 2026, 2 * 4, {"mb": K.flash_mask_bank(64)}),
+    "flash_causal_bh2_s256_d64": (K.flash_src(2, 256, 64, 64, causal=True), 2026, 2 * 4,
+                                  {"mb": K.flash_mask_bank(64)}),
+    # the shipped integer max-shift attention kernel, verbatim (ref proj/kernels/attention.k)
+    "attention_shipped": (K.shipped("attention.k"), 2026, 4, {}),
 }
 
 
 def main() -> None:
+    only = set(sys.argv[1:])
     for name, (src, seed, pids, extra) in CASES.items():
+        if only and name not in only:
+            continue
         rk = oracle.RefKernel(src)
         ins = rk.generate(seed)
         ins.update(extra)

@@ -18,7 +18,8 @@ def _declared_functions():
 
 def test_header_declares_the_path():
     assert _declared_functions() == ["ws_attn_fwd", "ws_attn_fwd_traced", "ws_debug_gemm_trace", "ws_gemm_tn", "ws_last_error",
-                                    "ws_launch_count", "ws_run_kernel", "ws_version", "ws_watchdog"]
+                                    "ws_launch_count", "ws_run_kernel", "ws_run_kernel_spec", "ws_version",
+                                    "ws_watchdog"]
 
 
 def test_library_exports_every_declared_symbol(ws):
@@ -45,7 +46,9 @@ def test_desc_layout_matches_header(tmp_path):
         pytest.skip("no host C compiler")
     lines = ['#include <stdio.h>', '#include <stddef.h>', f'#include "{os.path.join(ROOT, "include", "ws.h")}"',
              "int main(void) {"]
-    for cname, py in (("ws_gemm_desc", _lib.GemmDesc), ("ws_attn_desc", _lib.AttnDesc)):
+    structs = (("ws_gemm_desc", _lib.GemmDesc), ("ws_attn_desc", _lib.AttnDesc), ("ws_runspec", _lib.RunSpec),
+               ("ws_kbuffer", _lib.KBuffer))
+    for cname, py in structs:
         lines.append(f'printf("{cname} size %zu\\n", sizeof({cname}));')
         for f, _ in py._fields_:
             lines.append(f'printf("{cname} {f} %zu\\n", offsetof({cname}, {f}));')
@@ -55,7 +58,7 @@ def test_desc_layout_matches_header(tmp_path):
     exe = tmp_path / "layout"
     subprocess.check_call([cc, "-o", str(exe), str(src)])
     got = dict((" ".join(l.split()[:2]), int(l.split()[2])) for l in subprocess.check_output([str(exe)], text=True).splitlines())
-    for cname, py in (("ws_gemm_desc", _lib.GemmDesc), ("ws_attn_desc", _lib.AttnDesc)):
+    for cname, py in structs:
         assert got[f"{cname} size"] == ctypes.sizeof(py)
         for f, _ in py._fields_:
             assert got[f"{cname} {f}"] == getattr(py, f).offset, (cname, f)

@@ -59,3 +59,46 @@ def test_flash_through_the_reference_flow(ws, dev, tmp_path, causal):
     rc, log = _run(tmp_path, [K.flash_src(2, 384, 64, 128, causal)], "--pids", "6", "--flash")
     assert rc == 0, log
     assert "PASS" in log, log
+
+
+def test_runspec_rejection_through_the_reference_flow(tmp_path):
+    """The reference's own RunSpec with P > D, set on ws::Launch from a warpspec::RunSpec, is rejected
+    by the GPU path with the reference's PipelineInfeasible before any device work (so this runs
+    on a CPU host too), exactly as compile_kernel rejects it (ref pipeline.hpp:84-92)."""
+    if not os.access(BIN, os.X_OK):
+        pytest.skip("oracle/_ref/ws_dropin not built (needs the reference headers at build time)")
+    rc, log = _run(tmp_path, [K.gemm_src(256, 256, 512, 128, 128, 64)], "--pids", "4", "--spec", "2,3,fine,1,0")
+    assert rc == 1 and "REJECTED" in log and "pipeline-infeasible" in log, log
+    rc, log = _run(tmp_path, [K.flash_src(2, 256, 64, 128, True)], "--pids", "4", "--flash", "--spec",
+                   "1,1,coarse,1,0")
+    assert rc == 1 and "pipeline-infeasible" in log, log
+
+
+@pytest.mark.gpu
+def test_attention_k_through_the_reference_flow(ws, dev, tmp_path):
+    """The shipped integer attention.k (text from the reference-made golden): generate_inputs,
+    interpret_tiles and ws::run agree exactly, also under the reference's default RunSpec."""
+    if not os.access(BIN, os.X_OK):
+        pytest.skip("oracle/_ref/ws_dropin not built (needs the reference headers at build time)")
+    import numpy as np
+
+    text = str(np.load(os.path.join(ROOT, "tests", "golden", "attention_shipped.npz"))["kernel"])
+    rc, log = _run(tmp_path, [text], "--pids", "4")
+    assert rc == 0 and "PASS" in log, log
+    rc, log = _run(tmp_path, [text], "--pids", "4", "--spec", "2,1,auto,1,0")
+    assert rc == 0 and "PASS" in log, log
+
+
+@pytest.mark.gpu
+def test_runspec_through_the_reference_flow(ws, dev, tmp_path):
+    """Feasible reference RunSpecs (fine D=4 P=2 persistent, none, coarse flash D=3) give the same
+    buffers as the reference interpreter."""
+    if not os.access(BIN, os.X_OK):
+        pytest.skip("oracle/_ref/ws_dropin not built (needs the reference headers at build time)")
+    rc, log = _run(tmp_path, [K.gemm_src(256, 256, 512, 128, 128, 64)], "--pids", "4", "--spec", "4,2,fine,2,1")
+    assert rc == 0 and "PASS" in log, log
+    rc, log = _run(tmp_path, [K.gemm_src(256, 256, 512, 128, 128, 64)], "--pids", "4", "--spec", "1,1,none,1,0")
+    assert rc == 0 and "PASS" in log, log
+    rc, log = _run(tmp_path, [K.flash_src(2, 256, 64, 128, True)], "--pids", "4", "--flash", "--spec",
+                   "3,1,coarse,1,0")
+    assert rc == 0 and "PASS" in log, log
