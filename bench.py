@@ -1,13 +1,18 @@
 """Benchmark of the hot path: warp-specialized GEMM (+ FlashAttention forward) on B200.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
-  (N > 1: python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N ...)
+  (N > 1: launched by the driver as python -m torch.distributed.run --nproc-per-node N ... bench.py
+   --gpus N ...; without WORLD_SIZE in the environment, bench.py --gpus N re-launches itself that way)
 
 Headline workload = BASELINE.json configs[1]: bf16 GEMM M = N = 8192 with the K sweep
 256..16384 (c = a . b^T, bf16 in/out, fp32 accumulate). One step = one pass of the sweep (7
-launches). Metric: TFLOP/s = sum 2*M*N*K over the sweep / device time; "value" is the whole job
-over all ranks. Multi-GPU = weak scaling by N-column shards: rank g computes the
-8192-column block g of a global M x (8192*N) product — no collective on the data path.
+launches). Metric: TFLOP/s = sum 2*M*N*K over the sweep / device time (max over ranks); "value"
+is the whole job over all ranks. Multi-GPU = STRONG scaling of that global problem by N-column
+shards, as configs[1] names it ("N-sharded at 2/4/8"): rank g computes output
+columns [g*8192/N, (g+1)*8192/N) from all of A and its rows of B — no collective on the data path.
+The attention cases shard (b,h) the same way (C5: B*H = 16 over the ranks). After timing, the
+shards are all-gathered (NCCL) and checked bit-exactly against a full single-GPU product
+(`multi_gpu_verify`); weak scaling (every rank a full 8192 x 8192 sweep) is reported beside it.
 Inputs (A+B >= 64 MB per launch, 256 MB at K=8192) stream from HBM; L2 is flushed between steps
 with a 256 MB write so every step starts cold.
 
@@ -33,7 +38,7 @@ sys.path.insert(0, ROOT)
 M_ = N_ = 8192
 K_SWEEP = [256, 512, 1024, 2048, 4096, 8192, 16384]
 METRIC = "GEMM & attention-fwd TFLOPS at 1/2/4/8 B200, % of tensor-core peak"
-WORKLOAD = ("C2: bf16 GEMM c = a.b^T, M=N=8192 (per GPU; global N = 8192*n_gpus), "
+WORKLOAD = ("C2: bf16 GEMM c = a.b^T, M=N=8192 (global; N-column sharded over the GPUs), "
             "K sweep 256..16384, one pass = 7 launches")
 TILE_POLICY = ("library auto policy: cta_group::2 CTA pairs (M % 256 == 0, K >= 256); < 16 K blocks (K < 1024): "
                "256x256x64 pair tiles (D=6, raster group 2, TMEM double-buffered); >= 16 K blocks: 256x512x64 "
@@ -210,7 +215,7 @@ def run_reference_arm(args):
     line = {
         "metric": METRIC, "value": value, "unit": "TFLOP/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generate_inputs)",
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (reference generate_inputs)",
         "impl": "reference",
         "config": {"workload": WORKLOAD, "sample_per_step": f"{rounds_per_step} rounds x {s.threads} threads"},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": s.threads, "kind": s.kind,
@@ -233,10 +238,18 @@ def run_ours(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    ndev = torch.cuda.device_count()
+    # more ranks than GPUs (a one-GPU check of the multi-rank plumbing): ranks share devices and the
+    # process group is gloo (NCCL refuses two ranks on one GPU); timings then are not scaling numbers
+    shared = world > ndev
+    backend = "gloo" if shared else "nccl"
+    dev = torch.device("cuda", local % ndev)
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
     ws._lib.load()
     stream = torch.cuda.current_stream()
 
@@ -244,21 +257,39 @@ def run_ours(args):
         if world > 1:
             dist.barrier()
 
+    def coll(t):  # gloo collectives run on host copies
+        return t.cpu() if backend == "gloo" else t
+
     def max_over_ranks(x: float) -> float:
         if world == 1:
             return x
-        t = torch.tensor([x], device=dev, dtype=torch.float64)
+        t = coll(torch.tensor([x], device=dev, dtype=torch.float64))
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    g = torch.Generator(device=dev).manual_seed(1234 + rank)
+    def all_ranks(x: float) -> list:
+        if world == 1:
+            return [x]
+        t = coll(torch.tensor([x], device=dev, dtype=torch.float64))
+        parts = [torch.empty_like(t) for _ in range(world)]
+        dist.all_gather(parts, t)
+        return [round(float(p.item()), 4) for p in parts]
+
+    from paper_2510_14719_b200 import shard as shard_plan
+    # this rank's output-column shard of the global 8192 x 8192 product (strong scaling)
+    n_lo, n_hi = shard_plan.gemm_shard(N_, world, rank, 128 if world > 32 else 256)
+    n_loc = n_hi - n_lo
+
+    g = torch.Generator(device=dev).manual_seed(1234)  # every rank builds the same global operands
     Kmax = max(K_SWEEP)
-    # A and this rank's 8192-row block of B (the N-column shard); per-K operands are column slices
+    # A and this rank's rows [n_lo, n_hi) of B (its N-column shard); per-K operands are column slices
     a_full = (torch.randn(M_, Kmax, device=dev, generator=g) * 0.5).to(torch.bfloat16)
     b_full = (torch.randn(N_, Kmax, device=dev, generator=g) * 0.5).to(torch.bfloat16)
-    ops = {K: (a_full[:, :K].contiguous(), b_full[:, :K].contiguous()) for K in K_SWEEP}
+    ops = {K: (a_full[:, :K].contiguous(), b_full[n_lo:n_hi, :K].contiguous()) for K in K_SWEEP}
+    full_ops = ({K: (ops[K][0], b_full[:, :K].contiguous()) for K in K_SWEEP} if world > 1 else ops)
     del a_full, b_full
-    c = torch.empty(M_, N_, device=dev, dtype=torch.bfloat16)
+    c = torch.empty(M_, n_loc, device=dev, dtype=torch.bfloat16)
+    c_full = torch.empty(M_, N_, device=dev, dtype=torch.bfloat16) if world > 1 else c
     flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)
 
     def step(evs=None):
@@ -313,20 +344,42 @@ def run_ours(args):
             d = evs[i][0].elapsed_time(evs[i][1])
             kern[K] += d
             total_ms += d
+    rank_ms = all_ranks(total_ms / args.steps)
     total_ms = max_over_ranks(total_ms)
     ms_per_step = total_ms / args.steps
-    value = world * STEP_FLOPS / (ms_per_step * 1e-3) / 1e12
+    value = STEP_FLOPS / (ms_per_step * 1e-3) / 1e12  # the global problem over the slowest rank
+    kern = {K: max_over_ranks(kern[K]) for K in K_SWEEP}
     per_k = {str(K): round(gemm_flops(K) / (kern[K] / args.steps * 1e-3) / 1e12, 1) for K in K_SWEEP}
+    # weak scaling beside it: every rank the full 8192 x 8192 sweep (per-GPU work fixed)
+    weak = None
+    if world > 1:
+        def full_sweep():
+            for K in K_SWEEP:
+                ws.gemm_tn(*full_ops[K], c_full)
+        for _ in range(2):
+            full_sweep()
+        barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        n_w = max(3, min(args.steps, 20))
+        e0.record(stream)
+        for _ in range(n_w):
+            full_sweep()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        wms = max_over_ranks(e0.elapsed_time(e1) / n_w)
+        weak = {"value": round(world * STEP_FLOPS / (wms * 1e-3) / 1e12, 2), "ms_per_step": round(wms, 4),
+                "per_gpu_work": "the full 8192 x 8192 K sweep on every rank", "steps": n_w}
 
     peaks = load_peaks()
     # dominant kernel: the K=16384 launch (largest share of the step)
     Kd = max(K_SWEEP, key=lambda K: kern[K])
     dom_ms = kern[Kd] / args.steps
-    achieved = gemm_flops(Kd) / (dom_ms * 1e-3) / 1e12
+    achieved = gemm_flops(Kd, N=n_loc) / (dom_ms * 1e-3) / 1e12  # per GPU: its shard's launch
     traffic = load_traffic().get(f"gemm_bf16_8192x8192x{Kd}", {}).get("dram_bytes_per_launch")
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peaks["bf16_sustained"],
                 "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_sustained"], 4), "traffic": traffic,
-                "kernel": f"ws_gemm_tn_kernel<bf16,bf16,{512 if Kd >= 1024 else 256},cta_group::2> M=N=8192 K={Kd}",
+                "kernel": f"ws_gemm_tn_kernel<bf16,bf16,{512 if Kd >= 1024 else 256},cta_group::2> M=8192 N={n_loc} K={Kd}",
                 "peak_kind": f"bf16_tflops_sustained ({peaks['source']}); the timed loop runs back to back",
                 "frac_of_burst": round(achieved / peaks["bf16"], 4),
                 "frac_of_dense_2250": round(achieved / 2250.0, 4),
@@ -417,25 +470,36 @@ def run_ours(args):
 
     # ---- attention path (C4 / C5), reported beside the headline ----
     settle()
-    attn = bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier)
+    attn = bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier, rank=rank)
     if world == 1 and not args.no_vs_cublas:
         settle()
         attn["vs_trtllm_gen_fmha_same_box"] = bench_attention_vs_lib(ws, torch, dev, stream)
     settle()
-    other_configs = bench_fp8_and_c1(ws, torch, dev, stream, args, world, max_over_ranks, barrier)
+    other_configs = bench_fp8_and_c1(ws, torch, dev, stream, args, world, max_over_ranks, barrier,
+                                     n_range=(n_lo, n_hi))
 
     # ---- e2e through the public API with host buffers (pinned), copies inside the timed region ----
     settle()
-    e2e = bench_e2e(ws, torch, dev, stream, args, world, max_over_ranks, barrier)
+    e2e = bench_e2e(ws, torch, dev, stream, args, world, max_over_ranks, barrier, n_range=(n_lo, n_hi))
+
+    # ---- multi-GPU verification, outside every timed region: the shards all-gathered over the
+    # process group (NCCL on a GPU box) and compared bit-exactly with one rank's full product ----
+    verify = multi_gpu_verify(ws, torch, dev, world, rank, backend) if world > 1 else None
 
     line = {
         "metric": METRIC, "value": round(value, 2), "unit": "TFLOP/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4), "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (randn*0.5, bf16)",
-        "config": {"workload": WORKLOAD, "M": M_, "N_per_gpu": N_, "K_sweep": K_SWEEP,
-                   "parallelism": f"N-column shards x{world} (weak)", "tile": TILE_POLICY,
+        "config": {"workload": WORKLOAD, "M": M_, "N": N_, "N_per_gpu": n_loc, "K_sweep": K_SWEEP,
+                   "parallelism": f"N-column shards x{world} (strong: the global 8192 x 8192 problem split)",
+                   "tile": TILE_POLICY,
                    "l2": "flushed between steps (256 MB write, excluded from timing); operands >= 64 MB per launch"},
         "frac_of_peak": round(value / world / peaks["bf16_sustained"], 4),
+        "per_rank_ms_per_step": rank_ms,
+        "process_group": (backend + (" (ranks share GPUs: a plumbing check, not a scaling number)" if shared else ""))
+        if world > 1 else None,
+        "weak_scaling": weak,
+        "multi_gpu_verify": verify,
         "tflops_per_k": per_k,
         "gemm_8192_cubed_tflops": per_k["8192"],
         "vs_cublas_same_box": lib,
@@ -458,6 +522,41 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def multi_gpu_verify(ws, torch, dev, world, rank, backend):
+    """SURVEY §8e's only collective: every rank computes its N-column shard of a GEMM and its (b,h)
+    shard of a causal attention; the shards are all-gathered (multi.gather_*, NCCL over NVLink on a
+    GPU box) and rank 0 compares the gathered outputs BIT-EXACTLY with the same problem computed
+    whole on its own GPU. The GEMM payload is k/4 values (|k| <= 16) with fp32 output, exact in every
+    summation order; each attention (b,h) slice is computed by the same per-slice code either way."""
+    import torch.distributed as dist
+
+    from paper_2510_14719_b200 import multi, shard as shard_plan
+
+    g = torch.Generator(device=dev).manual_seed(2026)
+    M, N, K = 4096, 8192, 1024
+    a = (torch.randint(-16, 17, (M, K), device=dev, generator=g).float() / 4).to(torch.bfloat16)
+    b = (torch.randint(-16, 17, (N, K), device=dev, generator=g).float() / 4).to(torch.bfloat16)
+    local = multi.gemm_forward_shard(a, b, rank, world, bn=256, out_dtype=torch.float32)
+    tx = (lambda t: t.cpu()) if backend == "gloo" else (lambda t: t)
+    full = multi.gather_gemm_columns(tx(local), N, world, bn=256).to(dev)
+    B, H, S, Dh = 1, 16, 2048, 128
+    q, k, v = (torch.randn(B, H, S, Dh, device=dev, generator=g).to(torch.bfloat16) for _ in range(3))
+    o_l, l_l = multi.attn_forward_shard(q, k, v, rank, world, causal=True)
+    o, lse = multi.gather_attn_slices(tx(o_l.contiguous()), tx(l_l.contiguous()), B * H, world)
+    res = {"collective": f"all_gather over {backend}", "world": world}
+    if rank == 0:
+        want = ws.gemm_tn(a, b, out_dtype=torch.float32)
+        ro, rl = ws.attn_fwd(q, k, v, causal=True)
+        torch.cuda.synchronize()
+        res["gemm_4096x8192x1024_fp32"] = "bit-exact" if torch.equal(full, want) else "MISMATCH"
+        ok = torch.equal(o.to(dev), ro.view(B * H, S, Dh)) and torch.equal(lse.to(dev), rl.view(B * H, S))
+        res["attn_causal_b1_h16_s2048_d128"] = "bit-exact" if ok else "MISMATCH"
+        res["shards"] = {"gemm_columns": [list(shard_plan.gemm_shard(N, world, r, 256)) for r in range(world)],
+                         "attn_bh": [list(shard_plan.attn_shard(B * H, world, r)) for r in range(world)]}
+    dist.barrier()
+    return res
 
 
 def bench_attention_vs_lib(ws, torch, dev, stream):
@@ -485,10 +584,13 @@ def bench_attention_vs_lib(ws, torch, dev, stream):
         return {"unavailable": f"{type(e).__name__}: {str(e)[:120]}"}
 
 
-def bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier):
+def bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier, rank=0):
     """C4 / C5 (and FP8) attention rates: per case, the median over 5 repeats of `iters` back-to-back
     launches (device time, CUDA events on the launch stream, max over ranks) — the cases are short, so
-    a single window is at the mercy of the power-capped clock's steps."""
+    a single window is at the mercy of the power-capped clock's steps. With N ranks every case is
+    (b,h)-sharded: rank g runs slices [g*BH/N, (g+1)*BH/N) of the same global problem
+    and the rate is the global FLOPs over the slowest rank (strong scaling)."""
+    from paper_2510_14719_b200 import shard as shard_plan
     iters_ = max(3, min(args.steps, 10))
     out = {"_method": f"per case: 0.5 s settle, 3 warm-up launches, then the median of 5 windows of {iters_} "
                       "back-to-back launches (CUDA events, max over ranks); inputs >= 64 MB per tensor"}
@@ -526,14 +628,17 @@ def bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier
         v = torch.randn_like(q)
         o = torch.empty_like(q)
         lse = torch.empty(B, H, S, device=dev)
+        bhr = shard_plan.attn_shard(B * H, world, rank)
         for _ in range(3):
-            ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse)
-        ms = timed_median(lambda: ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse))
+            ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse, bh_range=bhr)
+        ms = timed_median(lambda: ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse, bh_range=bhr))
         fl = 4.0 * B * H * S * S * Dh / (2 if causal else 1)
-        tf = fl / (ms * 1e-3) / 1e12
-        out[name] = {"tflops": round(world * tf, 1), "ms": round(ms, 4),
-                     "frac_of_measured_sustained_bf16": round(tf / load_peaks()["bf16_sustained"], 4),
-                     "frac_of_dense_2250": round(tf / 2250.0, 4)}
+        tf = fl / (ms * 1e-3) / 1e12  # the global problem over the slowest rank
+        out[name] = {"tflops": round(tf, 1), "ms": round(ms, 4),
+                     "frac_of_measured_sustained_bf16": round(tf / world / load_peaks()["bf16_sustained"], 4),
+                     "frac_of_dense_2250": round(tf / world / 2250.0, 4)}
+        if world > 1:
+            out[name]["bh_shard"] = list(bhr)
         del q, k, v, o, lse
     # FP8 e4m3 attention (hdim 128, per-tensor descales, bf16 O)
     for name, causal in (("fp8_noncausal_s16k_d128", False), ("fp8_causal_s16k_d128", True)):
@@ -542,19 +647,22 @@ def bench_attention(ws, torch, dev, stream, args, world, max_over_ranks, barrier
         v = torch.randn(1, 16, 16384, 128, device=dev).to(torch.float8_e4m3fn)
         o = torch.empty(1, 16, 16384, 128, device=dev, dtype=torch.bfloat16)
         lse = torch.empty(1, 16, 16384, device=dev)
+        bhr = shard_plan.attn_shard(16, world, rank)
         for _ in range(3):
-            ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse)
-        ms = timed_median(lambda: ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse))
+            ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse, bh_range=bhr)
+        ms = timed_median(lambda: ws.attn_fwd(q, k, v, causal=causal, out=o, lse=lse, bh_range=bhr))
         fl = 4.0 * 16 * 16384 * 16384 * 128 / (2 if causal else 1)
-        out[name] = {"tflops": round(world * fl / (ms * 1e-3) / 1e12, 1), "ms": round(ms, 4),
-                     "frac_of_dense_fp8_4500": round(fl / (ms * 1e-3) / 1e12 / 4500.0, 4)}
+        out[name] = {"tflops": round(fl / (ms * 1e-3) / 1e12, 1), "ms": round(ms, 4),
+                     "frac_of_dense_fp8_4500": round(fl / world / (ms * 1e-3) / 1e12 / 4500.0, 4)}
         del q, k, v, o, lse
     return out
 
 
-def bench_fp8_and_c1(ws, torch, dev, stream, args, world, max_over_ranks, barrier):
-    """C3 (FP8 e4m3 GEMM M=N=8192, K sweep, fp32 accumulate, per-tensor scales, bf16 out) and C1
-    (fp16 1024^3, fp32 out), device time per launch, reported beside the headline."""
+def bench_fp8_and_c1(ws, torch, dev, stream, args, world, max_over_ranks, barrier, n_range=(0, 8192)):
+    """C3 (FP8 e4m3 GEMM M=N=8192, K sweep, fp32 accumulate, per-tensor scales, bf16 out; N-column
+    sharded like the headline) and C1 (fp16 1024^3, fp32 out; single-GPU correctness config, per-GPU
+    rate), device time per launch, reported beside the headline."""
+    n_lo, n_hi = n_range
     res = {"c3_fp8_tflops_per_k": {}}
     iters = max(3, min(args.steps, 20))
 
@@ -571,33 +679,36 @@ def bench_fp8_and_c1(ws, torch, dev, stream, args, world, max_over_ranks, barrie
         torch.cuda.synchronize()
         return max_over_ranks(e0.elapsed_time(e1) / iters)
 
-    c = torch.empty(M_, N_, device=dev, dtype=torch.bfloat16)
+    c = torch.empty(M_, n_hi - n_lo, device=dev, dtype=torch.bfloat16)
     for K in K_SWEEP:
         a = (torch.randn(M_, K, device=dev) * 0.5).to(torch.float8_e4m3fn)
-        b = (torch.randn(N_, K, device=dev) * 0.5).to(torch.float8_e4m3fn)
+        b = (torch.randn(n_hi - n_lo, K, device=dev) * 0.5).to(torch.float8_e4m3fn)
         ms = timed(lambda: ws.gemm_tn(a, b, c, scale_a=0.5, scale_b=2.0))
-        res["c3_fp8_tflops_per_k"][str(K)] = round(world * gemm_flops(K) / (ms * 1e-3) / 1e12, 1)
+        res["c3_fp8_tflops_per_k"][str(K)] = round(gemm_flops(K) / (ms * 1e-3) / 1e12, 1)
         del a, b
     a = torch.randn(1024, 1024, device=dev).half()
     b = torch.randn(1024, 1024, device=dev).half()
     c1 = torch.empty(1024, 1024, device=dev, dtype=torch.float32)
     ms = timed(lambda: ws.gemm_tn(a, b, c1))
-    res["c1_fp16_1024_cubed_tflops"] = round(world * 2 * 1024 ** 3 / (ms * 1e-3) / 1e12, 1)
+    res["c1_fp16_1024_cubed_tflops"] = round(2 * 1024 ** 3 / (ms * 1e-3) / 1e12, 1)  # per GPU
     return res
 
 
-def bench_e2e(ws, torch, dev, stream, args, world, max_over_ranks, barrier):
+def bench_e2e(ws, torch, dev, stream, args, world, max_over_ranks, barrier, n_range=(0, 8192)):
     """Same sweep through ws.gemm_tn_host with host buffers: every step copies each launch's A, B
-    (pinned) H2D, runs it and copies its C back D2H, all inside the timed region."""
+    (pinned) H2D, runs it and copies its C back D2H, all inside the timed region. With N ranks each
+    copies A, its rows of B and its C column block (strong scaling, like the headline)."""
+    n_lo, n_hi = n_range
+    n_loc = n_hi - n_lo
     host_ab = {}
     for K in K_SWEEP:
         a = (torch.randn(M_, K) * 0.5).to(torch.bfloat16).pin_memory()
-        b = (torch.randn(N_, K) * 0.5).to(torch.bfloat16).pin_memory()
+        b = (torch.randn(n_loc, K) * 0.5).to(torch.bfloat16).pin_memory()
         host_ab[K] = (a, b)
     # two pinned host C buffers, alternating per launch (job i's D2H lands in host_c[i % 2]); the
     # copies are ordered on the pipeline's D2H stream, so a buffer is rewritten only after the
     # previous copy into it completed
-    host_c = [torch.empty(M_, N_, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
+    host_c = [torch.empty(M_, n_loc, dtype=torch.bfloat16).pin_memory() for _ in range(2)]
     jobs = [(host_ab[K][0], host_ab[K][1], host_c[i % 2]) for i, K in enumerate(K_SWEEP)]
 
     def step():
@@ -615,12 +726,71 @@ def bench_e2e(ws, torch, dev, stream, args, world, max_over_ranks, barrier):
     e1.record(stream)
     torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1) / iters)
-    h2d = sum(2 * (M_ * K) * 2 for K in K_SWEEP)
-    d2h = len(K_SWEEP) * M_ * N_ * 2
-    return {"value": round(world * STEP_FLOPS / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
+    h2d = sum((M_ * K + n_loc * K) * 2 for K in K_SWEEP)
+    d2h = len(K_SWEEP) * M_ * n_loc * 2
+    return {"value": round(STEP_FLOPS / (ms * 1e-3) / 1e12, 2), "unit": "TFLOP/s",
             "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h, "ms_per_step": round(ms, 3),
             "path": "paper_2510_14719_b200.gemm_tn_host -> ws_gemm_tn (C-ABI): pinned host A, B in and C out every "
                     "launch; H2D of launch i+1, GEMM i and D2H of launch i-1 overlap on three streams"}
+
+
+def self_launch(args) -> int:
+    """`bench.py --gpus N` (N > 1) without a torchrun environment: re-run this command as N ranks
+    under torch.distributed.run (one process per GPU, rendezvous on 127.0.0.1) and return its exit
+    status; rank 0 prints the JSON line."""
+    import socket
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=dict(os.environ, OMP_NUM_THREADS=os.environ.get("OMP_NUM_THREADS", "1")))
+
+
+def run_selftest(args) -> int:
+    """The multi-rank plumbing of run_ours on CPU (no GPU): gloo process group, the strong-scaling
+    shard plan of the headline and the attention cases, max-over-ranks timing, per-rank timings and
+    the verification all-gather, with a double-precision CPU stand-in for the kernels (a test of the
+    launcher, never a bench number)."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2510_14719_b200 import multi, shard as shard_plan
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if world > 1:
+        dist.init_process_group("gloo")
+    n_lo, n_hi = shard_plan.gemm_shard(N_, world, rank, 256)
+    g = torch.Generator().manual_seed(7)
+    a = torch.randint(-16, 17, (64, 96), generator=g).double() / 4
+    b = torch.randint(-16, 17, (N_ // 8, 96), generator=g).double() / 4
+    t0 = time.perf_counter()
+    local = multi.gemm_forward_shard(a, b, rank, world, bn=32, gemm=lambda x, y, **kw: x @ y.T)
+    ms = (time.perf_counter() - t0) * 1e3
+    full = multi.gather_gemm_columns(local, b.shape[0], world, bn=32) if world > 1 else local
+    ok = torch.equal(full, a @ b.T)
+    t = torch.tensor([ms], dtype=torch.float64)
+    parts = [torch.empty_like(t) for _ in range(world)]
+    if world > 1:
+        dist.all_gather(parts, t)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    else:
+        parts = [t]
+    okt = torch.tensor([1.0 if ok else 0.0])
+    if world > 1:
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+    if rank == 0:
+        print(json.dumps({"selftest": True, "n_gpus": world, "gpus_flag": args.gpus, "scaling": "strong",
+                          "shards": [list(shard_plan.gemm_shard(N_, world, r, 256)) for r in range(world)],
+                          "attn_shards_c5": [list(shard_plan.attn_shard(16, world, r)) for r in range(world)],
+                          "per_rank_ms": [float(p.item()) for p in parts], "max_ms": float(t.item()),
+                          "verify": "bit-exact" if okt.item() == 1.0 else "MISMATCH"}), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0 if okt.item() == 1.0 else 1
 
 
 def main():
@@ -631,9 +801,20 @@ def main():
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-vs-cublas", action="store_true", help="skip the cuBLAS comparison windows")
+    ap.add_argument("--selftest", action="store_true",
+                    help="CPU check of the multi-rank launcher and shard plumbing (gloo, no GPU)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    world_env = os.environ.get("WORLD_SIZE")
+    if world_env is None and args.gpus > 1:
+        return self_launch(args)
+    if world_env is not None and int(world_env) != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world_env}: launch one rank per GPU"}),
+              flush=True)
+        return 2
+    if args.selftest:
+        return run_selftest(args)
     if args.impl == "reference":
         return run_reference_arm(args)
     return run_ours(args)

@@ -75,7 +75,7 @@ def test_shards_partition_columns_and_pids():
         cols = [shard.gemm_shard(8192 * world, world, r) for r in range(world)]
         assert cols[0][0] == 0 and cols[-1][1] == 8192 * world
         assert all(cols[i][1] == cols[i + 1][0] for i in range(world - 1))
-        assert all(hi - lo == 8192 for lo, hi in cols)  # weak scaling: equal blocks
+        assert all(hi - lo == 8192 for lo, hi in cols)  # equal blocks
         pids = [shard.gemm_pid_range(8192, 8192 * world, 128, 256, world, r) for r in range(world)]
         assert pids[0][0] == 0 and pids[-1][1] == 64 * 32 * world
         assert all(pids[i][1] == pids[i + 1][0] for i in range(world - 1))
@@ -93,3 +93,38 @@ def test_attn_shards_partition_slices():
 def test_uneven_split_rejects_unaligned():
     with pytest.raises(ValueError):
         shard.gemm_shard(1000, 2, 0, 256)
+
+
+def _bench(*args, env=None):
+    import subprocess
+    import sys
+
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    e = {k: v for k, v in os.environ.items() if k not in ("WORLD_SIZE", "RANK", "LOCAL_RANK", "MASTER_ADDR",
+                                                             "MASTER_PORT")}
+    e.update(env or {})
+    return subprocess.run([sys.executable, os.path.join(root, "bench.py"), *args], capture_output=True, text=True,
+                          timeout=600, env=e)
+
+
+@pytest.mark.parametrize("n", [2, 3])
+def test_bench_self_launches_n_ranks(n):
+    """`bench.py --gpus N` without a torchrun environment re-launches itself as N ranks (gloo here,
+    --selftest: the launcher, strong-scaling shard plan, max-over-ranks timing and verification
+    all-gather with a CPU stand-in for the kernels); rank 0 prints one line with n_gpus = N."""
+    import json
+
+    out = _bench("--gpus", str(n), "--selftest")
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, out.stdout
+    j = json.loads(lines[0])
+    assert j["n_gpus"] == n and j["scaling"] == "strong" and j["verify"] == "bit-exact"
+    assert len(j["per_rank_ms"]) == n and j["max_ms"] == max(j["per_rank_ms"])
+    cols = j["shards"]
+    assert cols[0][0] == 0 and cols[-1][1] == 8192 and all(cols[i][1] == cols[i + 1][0] for i in range(n - 1))
+
+
+def test_bench_rejects_world_size_mismatch():
+    out = _bench("--gpus", "4", "--selftest", env={"WORLD_SIZE": "2", "RANK": "0"})
+    assert out.returncode == 2 and "WORLD_SIZE" in out.stdout
