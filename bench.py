@@ -23,6 +23,7 @@ the CPU baseline (the reference's own interpret_sequential from oracle/_ref when
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import math
 import os
@@ -178,7 +179,100 @@ class CpuSampler:
                 f"rate extrapolates linearly in tiles and K to the full M=N=8192 sweep")
 
 
-def cpu_baseline(budget_s: float = 12.0):
+def _cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for ln in f:
+                if ln.startswith("model name"):
+                    return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
+def _threaded(fns, threads):
+    """Run the unit callables fns[0..threads) once each on `threads` host threads; wall seconds.
+    (The reference's interpreter is a ctypes call, which releases the GIL.)"""
+    ths = [threading.Thread(target=fns[i % len(fns)]) for i in range(threads)]
+    t0 = time.perf_counter()
+    for t in ths:
+        t.start()
+    for t in ths:
+        t.join()
+    return time.perf_counter() - t0
+
+
+def cpu_configs(threads: int) -> dict:
+    """The other BASELINE configs on the host cores (BASELINE.md CPU plan), each through the
+    reference's own interpret_sequential (oracle/_ref) when built, else the C port:
+      C1  in full: all 32 pids of gemm.k 1024^3 (128x256x64 tiles), pid ranges over the threads, the
+          as-shipped per-pid flow (whole-buffer copies included); and the same on ONE thread
+          (interpret_tiles as the reference's tests run it, ref tests/support/fixtures.hpp:148-157)
+      C3  the FP8 GEMM: on the CPU the same double arithmetic as C2 (the reference has no FP8), one
+          panel-local 128x256 tile over a K=1024 slab per thread, extrapolated like C2
+      C4/C5  panel-local flash .k q-blocks (128 query rows against all S keys of one (b,h)), one per
+          thread per round, extrapolated linearly to B*H*S/128 q-blocks; the causal .k masks instead
+          of skipping (as the reference does), so its time per q-block is the non-causal one while
+          its useful FLOPs are half"""
+    import numpy as np
+
+    import oracle
+    from oracle import kernels as K
+
+    if not oracle.ref_available():
+        return {"unavailable": "oracle/_ref not built; the C port covers the headline sample only"}
+    res = {}
+    # C1 in full, all threads, then one thread as shipped
+    src = K.gemm_src(1024, 1024, 1024, 128, 256, 64)
+    rk = oracle.RefKernel(src)
+    ins = rk.generate()
+    npid = 32
+    nt = min(threads, npid)
+    ranges = [(npid * t // nt, npid * (t + 1) // nt) for t in range(nt)]
+    wall = _threaded([(lambda lo=lo, hi=hi: rk.run(ins, lo, hi)) for lo, hi in ranges], nt)
+    res["c1_fp16_1024_cubed"] = {"tflops": round(2 * 1024 ** 3 / wall / 1e12, 6), "wall_s": round(wall, 3),
+                                 "threads": nt, "sample": "the whole config: 32 pids of gemm.k (128x256x64 tiles)"}
+    t0 = time.perf_counter()
+    rk.run(ins, 0, npid)
+    t1 = time.perf_counter() - t0
+    res["c1_single_thread_as_shipped"] = {"tflops": round(2 * 1024 ** 3 / t1 / 1e12, 6), "wall_s": round(t1, 3),
+                                          "threads": 1}
+    # C3: panel-local tile units, like the headline
+    s3 = CpuSampler(threads=threads)
+    s3.round()
+    rounds, wall = 0, 0.0
+    while wall < 2.0 and rounds < 50:
+        wall += s3.round()
+        rounds += 1
+    res["c3_fp8_gemm_8192_sweep"] = {"tflops": round(rounds * threads * s3.flops_per_unit / wall / 1e12, 6),
+                                     "wall_s": round(wall, 3), "threads": threads,
+                                     "sample": f"{rounds} rounds x {threads} panel-local 128x256 tiles, K=1024 slab"}
+    # C4 / C5: q-block units
+    cases = [("c4_noncausal_s16k_d128", 1, 16, 16384, 128, False), ("c4_noncausal_s1k_d128_b16", 16, 16, 1024, 128, False),
+             ("c5_causal_s16k_d128", 1, 16, 16384, 128, True), ("c5_causal_s16k_d64", 1, 16, 16384, 64, True)]
+    rng = np.random.default_rng(2026)
+    for name, B, H, S, Dh, causal in cases:
+        nqb = S // 128
+        qbs = [int(x) for x in rng.integers(0, nqb, size=threads)] if causal else [0] * threads
+        kerns = [oracle.RefKernel(K.flash_block_src(S, Dh, 128, causal=causal, qb=qb)) for qb in sorted(set(qbs))]
+        by_qb = dict(zip(sorted(set(qbs)), kerns))
+        ins = kerns[0].generate()
+        if causal:
+            ins["mb"] = K.flash_mask_bank(128)
+        fns = [(lambda kk=by_qb[qb]: kk.run(ins, 0, 1)) for qb in qbs]
+        _threaded(fns[:1], 1)  # warm
+        wall = _threaded(fns, threads)
+        units_total = B * H * nqb
+        t_total = wall * units_total / threads
+        useful = 4.0 * B * H * S * S * Dh / (2 if causal else 1)
+        res[name] = {"tflops": round(useful / t_total / 1e12, 6), "threads": threads, "wall_s": round(wall, 3),
+                     "sample": f"{threads} panel-local 128-row q-blocks (one round), extrapolated to {units_total}"
+                               + (" (positions drawn at random; the .k masks, so cost is position-free)" if causal else "")}
+    return res
+
+
+def cpu_baseline(budget_s: float = 8.0):
     s = CpuSampler()
     s.round()  # warm
     rounds, wall = 0, 0.0
@@ -186,8 +280,13 @@ def cpu_baseline(budget_s: float = 12.0):
         wall += s.round()
         rounds += 1
     v = rounds * s.threads * s.flops_per_unit / wall / 1e12
-    return {"value": v, "unit": "TFLOP/s", "cores": s.threads, "kind": s.kind, "sample": s.sample_desc(rounds),
-            "wall_s": round(wall, 3)}
+    out = {"value": v, "unit": "TFLOP/s", "cores": s.threads, "kind": s.kind, "sample": s.sample_desc(rounds),
+           "wall_s": round(wall, 3), "cpu_model": _cpu_model(), "nproc": os.cpu_count()}
+    try:
+        out["configs"] = cpu_configs(s.threads)
+    except Exception as e:  # noqa: BLE001 — the side configs are reported, never required
+        out["configs"] = {"unavailable": f"{type(e).__name__}: {str(e)[:160]}"}
+    return out
 
 
 def run_reference_arm(args):
@@ -219,7 +318,8 @@ def run_reference_arm(args):
         "impl": "reference",
         "config": {"workload": WORKLOAD, "sample_per_step": f"{rounds_per_step} rounds x {s.threads} threads"},
         "cpu_baseline": {"value": value, "unit": "TFLOP/s", "cores": s.threads, "kind": s.kind,
-                         "sample": s.sample_desc(rounds_per_step * args.steps)},
+                         "sample": s.sample_desc(rounds_per_step * args.steps), "cpu_model": _cpu_model(),
+                         "nproc": os.cpu_count()},
         "e2e": {"value": value, "unit": "TFLOP/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -312,6 +412,10 @@ def run_ours(args):
         sampler.start()
         barrier()
         torch.cuda.synchronize()
+        # clock probe: each GEMM's CTA 0 stamps {%clock64, %globaltimer} at start and retirement;
+        # the last launch of the region (the dominant K = 16384 one) is read afterwards
+        clk_buf.zero_()
+        ws._lib.load().ws_debug_gemm_clock(ctypes.c_void_p(clk_buf.data_ptr()))
         launches0 = ws.launch_count()
         per_step = []
         for _ in range(args.steps):
@@ -321,8 +425,11 @@ def run_ours(args):
             per_step.append(evs)
         torch.cuda.synchronize()
         launches = ws.launch_count() - launches0
+        ws._lib.load().ws_debug_gemm_clock(None)
         barrier()
         return per_step, launches, sampler.stop()
+
+    clk_buf = torch.zeros(4, dtype=torch.int64, device=dev)
 
     def rejected(clk):
         # hardware / thermal slowdown, or SM clocks far below max with no reason (a leftover lock)
@@ -376,20 +483,34 @@ def run_ours(args):
     Kd = max(K_SWEEP, key=lambda K: kern[K])
     dom_ms = kern[Kd] / args.steps
     achieved = gemm_flops(Kd, N=n_loc) / (dom_ms * 1e-3) / 1e12  # per GPU: its shard's launch
-    traffic = load_traffic().get(f"gemm_bf16_8192x8192x{Kd}", {}).get("dram_bytes_per_launch")
-    roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peaks["bf16_sustained"],
-                "unit": "TFLOP/s", "frac": round(achieved / peaks["bf16_sustained"], 4), "traffic": traffic,
+    traffic = load_traffic().get(f"gemm_bf16_8192x{n_loc}x{Kd}", {}).get("dram_bytes_per_launch")
+    # peak by the timed region's length (B200_PROFILING.md): a region well under a second runs at
+    # burst clocks (the measured burst bf16 rate), a long one at the power-capped sustained rate
+    region_ms = ms_per_step * args.steps
+    burst = region_ms < 1000.0
+    peak = peaks["bf16"] if burst else peaks["bf16_sustained"]
+    roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
+                "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
                 "kernel": f"ws_gemm_tn_kernel<bf16,bf16,{512 if Kd >= 1024 else 256},cta_group::2> M=8192 N={n_loc} K={Kd}",
-                "peak_kind": f"bf16_tflops_sustained ({peaks['source']}); the timed loop runs back to back",
+                "peak_kind": (f"bf16_tflops {'burst' if burst else 'sustained'} ({peaks['source']}): the timed "
+                              f"region is {region_ms:.0f} ms"),
                 "frac_of_burst": round(achieved / peaks["bf16"], 4),
+                "frac_of_sustained": round(achieved / peaks["bf16_sustained"], 4),
                 "frac_of_dense_2250": round(achieved / 2250.0, 4),
                 "share_of_step": round(dom_ms / ms_per_step, 3)}
-    # the GPU is power-capped under sustained tensor load, so also state the dense bf16 peak at the
-    # SM clock sampled during the timed region (148 SMs x 8192 FLOP/clk): the per-clock efficiency
-    if clocks.get("sm_mhz"):
-        clk_peak = 148 * 8192 * clocks["sm_mhz"] * 1e6 / 1e12
-        roofline["peak_at_sampled_clock"] = round(clk_peak, 1)
-        roofline["frac_at_sampled_clock"] = round(achieved / clk_peak, 4)
+    if traffic is None:
+        roofline["traffic_note"] = "no ncu --set full summary of this shard shape in profiles/ncu_summary.json"
+    # per-clock efficiency from the dominant launch's own stamps: its CTA 0's %clock64 over
+    # %globaltimer gives the SM clock it ran at; dense bf16 peak at that clock = 148 SMs x 8192
+    # FLOP/clk (the nvidia-smi median below samples the whole region every 100 ms)
+    cs = clk_buf.cpu().tolist()
+    if cs[3] > cs[1] and cs[2] > cs[0]:
+        f_mhz = (cs[2] - cs[0]) / (cs[3] - cs[1]) * 1e3
+        clk_peak = 148 * 8192 * f_mhz * 1e6 / 1e12
+        roofline["kernel_sm_mhz"] = round(f_mhz, 1)
+        roofline["peak_at_kernel_clock"] = round(clk_peak, 1)
+        roofline["frac_at_kernel_clock"] = round(achieved / clk_peak, 4)
+        roofline["kernel_clock_source"] = "the last K=%d launch of the region: CTA 0 %%clock64 / %%globaltimer" % Kd
 
     # ---- the vendor library on the two dominant GEMM shapes, same box and power state (context
     # for the headline; not part of `value`) ----

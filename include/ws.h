@@ -209,6 +209,12 @@ int32_t ws_watchdog(ws_watchdog_info* out);
  * it off. Event map in csrc/gemm_sm100.cuh (GT); reader: scripts/gemm_trace.py. */
 void ws_debug_gemm_trace(unsigned long long* trace);
 
+/* Developer diagnostics: subsequent ws_gemm_tn launches have CTA 0 store {%clock64, %globaltimer}
+ * at its start and when it retires into `clk` (a device buffer of 4 uint64; the last launch's
+ * stamps win), so the SM clock a launch ran at is (clk[2]-clk[0]) / (clk[3]-clk[1]) GHz — the
+ * per-clock efficiency of a measured kernel without an external sampler. NULL turns it off. */
+void ws_debug_gemm_clock(unsigned long long* clk);
+
 #ifdef __cplusplus
 }
 #endif

@@ -130,14 +130,26 @@ def flash_mask_bank(BR: int):
     return mb
 
 
-def flash_block_src(S: int, D: int, BR: int, scale: float | None = None) -> str:
+def flash_block_src(S: int, D: int, BR: int, scale: float | None = None, causal: bool = False, qb: int = 0) -> str:
     """Panel-local flash .k: ONE BR-row query block against S keys (q is only BR rows), the unit
     the CPU baseline times so per-pid whole-buffer copies (ref interp.hpp:140-154) do not
-    dominate (CPU baseline plan)."""
+    dominate (CPU baseline plan). causal: the block sits at query-block position qb
+    and takes its score accumulator from the mask bank `mb` exactly as the batched causal .k
+    (SURVEY App. A selector sel = x/NB + (x-1)/NB, x = j - qb + NB); like the reference, it
+    masks instead of skipping, so its cost does not depend on qb."""
     BC = BR
     sc = scale if scale is not None else 1.0 / math.sqrt(D)
+    nb = S // BC
+    mb_param = f", mb: buf<{BR}x{3 * BC} real>" if causal else ""
+    if causal:
+        qk = [f"    %x0 = sub %j, {qb}", f"    %x = add %x0, {nb}", f"    %s0 = div %x, {nb}",
+              "    %xm = sub %x, 1", f"    %s1 = div %xm, {nb}", "    %sel = add %s0, %s1",
+              f"    %mc = mul %sel, {BC}", f"    %tm = tma_load mb[0, %mc] : {BR}x{BC} real",
+              "    %s = dot %tq, %tk.T, acc=%tm"]
+    else:
+        qk = ["    %s = dot %tq, %tk.T, acc=%zs"]
     return "\n".join([
-        f"kernel flash_block(q: buf<{BR}x{D} real>, k: buf<{S}x{D} real>, v: buf<{S}x{D} real>, "
+        f"kernel flash_block(q: buf<{BR}x{D} real>, k: buf<{S}x{D} real>, v: buf<{S}x{D} real>{mb_param}, "
         f"o: buf<{BR}x{D} real>, lsum: buf<{BR}x1 real>, mx: buf<{BR}x1 real>) {{",
         f"  %zacc = const zeros : {BR}x{D} real",
         f"  %zc = const zeros : {BR}x1 real",
@@ -149,7 +161,7 @@ def flash_block_src(S: int, D: int, BR: int, scale: float | None = None) -> str:
         f"  loop %j in 0..{S // BC} iter (%acc = %zacc, %m = %m0, %l = %zc, %ok = %k0) {{",
         f"    %tq = tma_load q[0, 0] : {BR}x{D} real",
         f"    %tk = tma_load k[%ok, 0] : {BC}x{D} real",
-        "    %s = dot %tq, %tk.T, acc=%zs",
+        *qk,
         f"    %tv = tma_load v[%ok, 0] : {BC}x{D} real",
         "    %ss = ew mul %s, %sc",
         "    %rm = reduce max %ss axis=1",

@@ -86,6 +86,7 @@ EXPORTS = {
     "ws_attn_fwd": (ctypes.c_int, [ctypes.POINTER(AttnDesc), ctypes.c_void_p]),
     "ws_attn_fwd_traced": (ctypes.c_int, [ctypes.POINTER(AttnDesc), ctypes.c_void_p, ctypes.c_void_p]),
     "ws_debug_gemm_trace": (None, [ctypes.c_void_p]),
+    "ws_debug_gemm_clock": (None, [ctypes.c_void_p]),
     "ws_watchdog": (ctypes.c_int32, [ctypes.c_void_p]),
     "ws_run_kernel": (ctypes.c_int, [ctypes.c_char_p, ctypes.POINTER(KBuffer), ctypes.c_int32, ctypes.c_int64,
                                      ctypes.c_int64, ctypes.c_int32, ctypes.c_void_p]),
@@ -97,7 +98,7 @@ EXPORTS = {
 }
 
 
-OPTIONAL = {"ws_debug_gemm_trace", "ws_watchdog"}
+OPTIONAL = {"ws_debug_gemm_trace", "ws_debug_gemm_clock", "ws_watchdog"}
 
 
 class WsError(RuntimeError):

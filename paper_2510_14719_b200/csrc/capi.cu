@@ -226,6 +226,7 @@ const int g_debug_deadlock = env_int("WS_DEBUG_DEADLOCK", 0);
 const bool g_trace_global = getenv("WS_GEMM_TRACE_GLOBAL") != nullptr;
 
 unsigned long long* g_gemm_trace = nullptr;  // ws_debug_gemm_trace
+unsigned long long* g_gemm_clk = nullptr;    // ws_debug_gemm_clock
 
 template <int IN, int OUT, int BN, int CG>
 ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
@@ -262,6 +263,7 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   p.scale = d.scale_a * d.scale_b;
   p.act = d.act;
   p.trace = g_gemm_trace;
+  p.clk = g_gemm_clk;
   // developer diagnostics: WS_DEBUG_DEADLOCK=1 makes CTA 0's producer skip its first aref put, so
   // the MMA warp waits forever and the watchdog fires (the simulator's Deadlock verdict on hardware)
   p.debug_deadlock = g_debug_deadlock;
@@ -610,6 +612,7 @@ int64_t ws_launch_count(void) { return g_launches.load(); }
 const char* ws_version(void) { return "ws-b200 0.1 sm_100a"; }
 
 void ws_debug_gemm_trace(unsigned long long* trace) { g_gemm_trace = trace; }
+void ws_debug_gemm_clock(unsigned long long* clk) { g_gemm_clk = clk; }
 
 int32_t ws_watchdog(ws_watchdog_info* out) {
   const volatile ws::WatchdogRecord* r = g_watchdog_host;

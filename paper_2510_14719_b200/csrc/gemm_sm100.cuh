@@ -49,6 +49,9 @@ struct GemmParams {
   int trace_global;  // stamps from %globaltimer (ns, comparable across SMs) instead of %clock64
   int debug_deadlock;  // WS_DEBUG_DEADLOCK: CTA 0 skips its first put (watchdog demonstration)
   int batch;           // independent products stacked along rows (gemm_batched.k); >= 1
+  // clock probe (ws_debug_gemm_clock): CTA 0 stores {%clock64, %globaltimer} when it starts and
+  // when it retires, so the SM clock during this launch is dclock / dns; nullptr = off
+  unsigned long long* clk;
 };
 
 struct GemmSmemLayout {
@@ -165,6 +168,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  if (p.clk && blockIdx.x == 0 && threadIdx.x == 64) {
+    p.clk[0] = clock64();
+    p.clk[1] = globaltimer();
+  }
   if (warp == 0) {
     // ===================== TMA producer: aref put =====================
     if (lane == 0) {
@@ -476,6 +483,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc<CG>(tmem_base, TMEM_COLS);
+  }
+  if (p.clk && blockIdx.x == 0 && threadIdx.x == 64) {
+    p.clk[2] = clock64();
+    p.clk[3] = globaltimer();
   }
 #undef GT
 }

@@ -17,7 +17,7 @@ def _declared_functions():
 
 
 def test_header_declares_the_path():
-    assert _declared_functions() == ["ws_attn_fwd", "ws_attn_fwd_traced", "ws_debug_gemm_trace", "ws_gemm_tn", "ws_last_error",
+    assert _declared_functions() == ["ws_attn_fwd", "ws_attn_fwd_traced", "ws_debug_gemm_clock", "ws_debug_gemm_trace", "ws_gemm_tn", "ws_last_error",
                                     "ws_launch_count", "ws_run_kernel", "ws_run_kernel_spec", "ws_version",
                                     "ws_watchdog"]
 
