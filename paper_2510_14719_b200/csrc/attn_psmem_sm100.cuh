@@ -42,29 +42,41 @@ namespace ws {
 // (measured, scripts/attn_ab.py: stagger + 1/8 beats 2/8 by 3-4% at hdim 128).
 constexpr int APS_POLY = 1;
 
+constexpr uint32_t APS_BAR_BYTES = (2 * A128_MAX_STAGES + 24) * 8;  // ring + per-tile / V barriers, TMEM slot
+
 __host__ __device__ inline uint32_t aps_smem_bytes(int Dh, int kv_stages) {
   // Q0 | Q1 | P0 | P1 | kv slots | barriers (+1 KB alignment slack)
-  return 2 * a128_q_bytes(Dh) + 2 * A128_BM * A128_BN * 2 + kv_stages * a128_kv_bytes(Dh) +
-         (2 * A128_MAX_STAGES + 16) * 8 + 16 + 1024;
+  return 2 * a128_q_bytes(Dh) + 2 * A128_BM * A128_BN * 2 + kv_stages * a128_kv_bytes(Dh) + APS_BAR_BYTES + 1024;
 }
 
-// FP8: Q, K, V in e4m3 (kind::f8f6f4 QK and PV, P quantized to e4m3 in shared memory, per-tensor
-// descales folded into the softmax scale and the epilogue), O in bf16.
+// FP8: Q, K, V in e4m3. QK^T runs in kind::f8f6f4; P stays 16-bit (f16 in shared memory) and PV
+// runs in kind::f16 against V converted e4m3 -> f16 in shared memory by two converter warps
+// (exact: every e4m3 value is an f16). V then has its own depth-2 aref with a transform stage:
+// TMA lands V_j (e4m3) in the upper half of f16 buffer j % 2 (vfull), the converter widens it in
+// place (each thread reads its whole 128-byte row before writing; f16 panel 1 of row r covers
+// exactly the bytes of e4m3 row r) and signals v16_full, PV_0(j) and PV_1(j) read it and commit
+// vempty. Every party walks every V position in order, so no parity test can alias; the K blocks
+// keep the ring (the MMA warp is their only consumer). Quantizing P itself to e4m3 (3 mantissa bits) left O up to
+// ~6% of max|V| off the fp32-accumulated oracle; f16 P keeps it at the 16-bit kernels' error.
+// Per-tensor descales fold into the softmax scale (q, k) and the epilogue (v); O in bf16.
 template <int DH, bool BF16, int POLY = 2, bool TRACE = false, bool FP8 = false>
 __global__ void __launch_bounds__(A128_THREADS, 1)
     ws_attn_psmem_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
                          const Attn128Params p) {
-  constexpr int EB = FP8 ? 1 : 2;                     // operand element bytes
+  constexpr int EB = FP8 ? 1 : 2;                     // Q / K / V element bytes
+  constexpr int PEB = 2;                              // P element bytes (16-bit, also for FP8)
   constexpr uint32_t QTILE = A128_BM * DH * EB;       // bytes of a 128 x DH Q tile
-  constexpr uint32_t PTILE = A128_BM * A128_BN * EB;  // bytes of a 128 x 128 P tile
+  constexpr uint32_t PTILE = A128_BM * A128_BN * PEB; // bytes of a 128 x 128 P tile
   constexpr uint32_t KVTILE = A128_BN * DH * EB;      // bytes of a 128 x DH K or V block
+  constexpr uint32_t V16TILE = FP8 ? A128_BN * DH * 2 : 0;  // FP8: a V block converted to f16
   constexpr uint32_t PANEL = 128 * 128;              // one 64-column (128 B) swizzle panel of 128 rows
   constexpr int NPANEL = DH * EB / 128;               // 128-byte panels per Q / K / V row
   constexpr int PANEL_ELEMS = 128 / EB;
-  constexpr uint32_t FMT = FP8 ? 0u : BF16 ? 1u : 0u;   // kind::f8f6f4 e4m3 / kind::f16 bf16, f16
-  constexpr uint32_t IDESC_QK = make_idesc(FMT, A128_BM, A128_BN, 0, 0);
-  constexpr uint32_t IDESC_PV = make_idesc(FMT, A128_BM, DH, 0, 1);  // A = P K-major, B = V MN-major
+  constexpr uint32_t FMT_QK = FP8 ? 0u : BF16 ? 1u : 0u;     // kind::f8f6f4 e4m3 / kind::f16 bf16, f16
+  constexpr uint32_t FMT_PV = (BF16 && !FP8) ? 1u : 0u;      // kind::f16: bf16, or f16 (FP8: f16 P, V)
+  constexpr uint32_t IDESC_QK = make_idesc(FMT_QK, A128_BM, A128_BN, 0, 0);
+  constexpr uint32_t IDESC_PV = make_idesc(FMT_PV, A128_BM, DH, 0, 1);  // A = P K-major, B = V MN-major
   constexpr uint32_t COL_O = 2 * A128_BN;
   constexpr uint32_t TMEM_COLS = 2 * A128_BN + 2 * DH <= 256 ? 256 : 512;
 
@@ -73,7 +85,8 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
   uint8_t* sq = smem;                  // Q0, Q1
   uint8_t* sp = smem + 2 * QTILE;      // P0, P1
   uint8_t* skv = sp + 2 * PTILE;       // K/V ring
-  uint8_t* bar_base = skv + p.kv_stages * KVTILE;
+  uint8_t* sv16 = skv + p.kv_stages * KVTILE;  // FP8: two f16 V buffers (the ring then holds K only)
+  uint8_t* bar_base = sv16 + 2 * V16TILE;
   auto* ring = reinterpret_cast<ArefBarriers<A128_MAX_STAGES>*>(bar_base);
   uint64_t* q_full = reinterpret_cast<uint64_t*>(bar_base + 2 * A128_MAX_STAGES * 8);
   uint64_t* s_full = q_full + 1;   // [2]
@@ -82,7 +95,10 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
   uint64_t* pv_done = q_full + 7;  // [2]
   uint64_t* o_free = q_full + 9;   // [2]
   uint64_t* q_free = q_full + 11;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 12);
+  uint64_t* v16_full = q_full + 12;   // [2] FP8: V_j converted to f16 (converter warps)
+  uint64_t* v16_empty = q_full + 14;  // [2] FP8: PV_0(j), PV_1(j) have read it (tcgen05.commit)
+  uint64_t* vfull = q_full + 16;      // [2] FP8: V_j (e4m3) landed (TMA transaction bytes)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(q_full + 18);
 
   const uint32_t warp = warp_id();
   const uint32_t lane = lane_id();
@@ -131,6 +147,9 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       mbar_init(&p_full[i], 4);
       mbar_init(&pv_done[i], 1);
       mbar_init(&o_free[i], 4);
+      mbar_init(&v16_full[i], 1);
+      mbar_init(&v16_empty[i], 1);
+      mbar_init(&vfull[i], 1);
     }
     fence_barrier_init();
   } else if (warp == 10) {
@@ -148,6 +167,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     regs_dec<72>();
     if (lane == 0) {
       ArefCursor c;
+      uint32_t vcnt = 0;  // FP8: V blocks put
       for (int it = 0, item = item_of(0); item < num_items; item = item_of(++it)) {
         int pair, bh;
         item_coords(item, pair, bh);
@@ -170,11 +190,22 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
             tma_load_2d(dst + h * PANEL, m, &ring->full[c.slot], h * PANEL_ELEMS, kv_row0 + blk * A128_BN);
           c.advance(D);
         };
+        // FP8: V_j -> the upper half of f16 buffer vcnt % 2, once PV_0, PV_1 of V_{j-2} are done
+        auto put_v = [&](int blk) {
+          const uint32_t b = vcnt & 1u;
+          mbar_wait(&v16_empty[b], ((vcnt >> 1) & 1u) ^ 1u, 10);
+          mbar_arrive_expect_tx(&vfull[b], KVTILE);
+          tma_load_2d(sv16 + b * V16TILE + V16TILE / 2, &tm_v, &vfull[b], 0, kv_row0 + blk * A128_BN);
+          ++vcnt;
+        };
         // ring order = MMA consumption order: K_0, then (K_{j+1}, V_j) for j = 0 .. n1-1
         put(&tm_k, 0);
         for (int j = 0; j < n1; ++j) {
           if (j + 1 < n1) put(&tm_k, j + 1);
-          put(&tm_v, j);
+          if constexpr (FP8)
+            put_v(j);
+          else
+            put(&tm_v, j);
         }
       }
     }
@@ -184,7 +215,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     const uint64_t qdesc = make_sw128_desc(smem_u32(sq), 16, 1024);
     const uint64_t pdesc = make_sw128_desc(smem_u32(sp), 16, 1024);
     const uint64_t kdesc = make_sw128_desc(smem_u32(skv), 16, 1024);
-    const uint64_t vdesc = make_sw128_desc(smem_u32(skv), PANEL, 1024);
+    const uint64_t vdesc = make_sw128_desc(smem_u32(FP8 ? sv16 : skv), PANEL, 1024);
     auto issue_qk = [&](int t, uint32_t k_slot) {
       const uint64_t a0 = qdesc + ((t * QTILE) >> 4), b0 = kdesc + ((k_slot * KVTILE) >> 4);
 #pragma unroll
@@ -197,21 +228,19 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       }
     };
     auto issue_pv = [&](int t, uint32_t v_slot, bool acc) {
-      const uint64_t a0 = pdesc + ((t * PTILE) >> 4), b0 = vdesc + ((v_slot * KVTILE) >> 4);
-      constexpr int KEYS = 32 / EB;  // keys per MMA (32 bytes of P)
+      // V from the K/V ring slot, or (FP8) from f16 buffer v_slot
+      const uint64_t a0 = pdesc + ((t * PTILE) >> 4), b0 = vdesc + ((v_slot * (FP8 ? V16TILE : KVTILE)) >> 4);
+      constexpr int KEYS = 32 / PEB;  // keys per MMA (32 bytes of P)
 #pragma unroll
       for (int k = 0; k < A128_BN / KEYS; ++k) {
         // A = P_t keys [KEYS k, KEYS (k+1)) (K-major, panel k/4); B = V rows of those keys
         // (MN-major, KEYS/8 eight-row core groups of 128 bytes)
         const uint32_t aoff = ((k / 4) * PANEL + (k % 4) * 32) >> 4;
-        if constexpr (FP8)
-          mma_f8_ss_warp(tmem + COL_O + t * DH, a0 + aoff, b0 + ((k * KEYS * 128) >> 4), IDESC_PV,
-                         (acc || k != 0) ? 1u : 0u);
-        else
-          mma_f16_ss_warp(tmem + COL_O + t * DH, a0 + aoff, b0 + ((k * KEYS * 128) >> 4), IDESC_PV,
-                          (acc || k != 0) ? 1u : 0u);
+        mma_f16_ss_warp(tmem + COL_O + t * DH, a0 + aoff, b0 + ((k * KEYS * 128) >> 4), IDESC_PV,
+                        (acc || k != 0) ? 1u : 0u);
       }
     };
+    uint32_t vcnt = 0;  // FP8: V blocks consumed (f16 buffer vcnt % 2, phase vcnt / 2 % 2)
     ArefCursor c;
     uint32_t g0 = 0, g1 = 0;  // blocks of tile 0 / tile 1 processed by earlier items
     // First QK of tile 0 of item `it` (K_0 taken from the ring, its slot kept for tile 1's QK). It
@@ -274,9 +303,15 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
           if (!p.stagger) qk1();
         }
         if (lane == 0) WS_TRACE(0, g1 + j, 2);
-        ring->get(c, 14);  // V_j
-        const uint32_t vslot = c.slot;
-        c.advance(D);
+        uint32_t vslot;
+        if constexpr (FP8) {
+          vslot = vcnt & 1u;  // V_j's f16 copy (the ring carries K only)
+          mbar_wait(&v16_full[vslot], (vcnt >> 1) & 1u, 14);
+        } else {
+          ring->get(c, 14);  // V_j
+          vslot = c.slot;
+          c.advance(D);
+        }
         if (j < n0) {
           mbar_wait(&p_full[0], (g0 + j) & 1, 15);  // C_0(j): P_0(j) in smem, O_0 rescaled
           if (j == 0 && it > 0) mbar_wait(&o_free[0], (it - 1) & 1, 19);  // previous O_0 copied out
@@ -299,11 +334,57 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         if (lane == 0) WS_TRACE(0, g1 + j, 4);
         issue_pv(1, vslot, j > 0);
         mma_commit_warp(&pv_done[1]);
-        mma_commit_warp(&ring->empty[vslot]);
+        if constexpr (FP8) {
+          mma_commit_warp(&v16_empty[vslot]);
+          ++vcnt;
+        } else {
+          mma_commit_warp(&ring->empty[vslot]);
+        }
         if (lane == 0) WS_TRACE(0, g1 + j, 5);
       }
       g0 += n0;
       g1 += n1;
+    }
+  } else if (FP8 && warp >= 10) {
+    // ===================== FP8: V converter (warps 10, 11) =====================
+    // V_j (e4m3, 128 keys x 128 B, SW128, in the upper half of f16 buffer vcnt % 2) -> f16 in the
+    // bf16 kernel's MN-major V layout (two 64-column SW128 panels), in place.
+    regs_dec<72>();
+    const uint32_t ct = (warp - 10u) * 32u + lane;  // 0..63: keys ct and ct + 64
+    uint32_t vcnt = 0;
+    for (int it = 0, item = item_of(0); item < num_items; item = item_of(++it)) {
+      int pair, bh;
+      item_coords(item, pair, bh);
+      const int n1 = nblk(pair, 1);
+      for (int j = 0; j < n1; ++j) {
+        const uint32_t b = vcnt & 1u;
+        mbar_wait(&vfull[b], (vcnt >> 1) & 1u, 30);  // V_j landed
+        const uint32_t dst = smem_u32(sv16 + b * V16TILE), src = dst + V16TILE / 2;
+#pragma unroll
+        for (int rr = 0; rr < 2; ++rr) {
+          const uint32_t r = ct + 64u * rr, sw = r & 7u;
+          uint4 x[8];  // the whole e4m3 row first: its f16 panel-1 half overwrites the same 128 bytes
+#pragma unroll
+          for (uint32_t cc = 0; cc < 8; ++cc) x[cc] = ld_shared_v4(src + r * 128u + ((cc ^ sw) << 4));
+#pragma unroll
+          for (uint32_t cc = 0; cc < 8; ++cc) {  // 16 e4m3 (head dims 16cc ..) -> two f16 chunks
+            const uint32_t xs[4] = {x[cc].x, x[cc].y, x[cc].z, x[cc].w};
+            uint32_t h[8];
+#pragma unroll
+            for (int w = 0; w < 4; ++w) {
+              h[2 * w] = e4m3x2_to_f16x2(xs[w] & 0xffffu);
+              h[2 * w + 1] = e4m3x2_to_f16x2(xs[w] >> 16);
+            }
+            const uint32_t row = dst + (cc / 4u) * PANEL + r * 128u, c8 = 2u * (cc % 4u);
+            st_shared_v4(row + ((c8 ^ sw) << 4), h[0], h[1], h[2], h[3]);
+            st_shared_v4(row + (((c8 + 1u) ^ sw) << 4), h[4], h[5], h[6], h[7]);
+          }
+        }
+        fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core's reads
+        named_bar_sync(3, 64);
+        if (ct == 0) mbar_arrive(&v16_full[b]);
+        ++vcnt;
+      }
     }
   } else if (warp >= 8) {
     regs_dec<72>();
@@ -429,7 +510,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       // 128B-swizzled K-major P tile as it is produced, so the shared-memory writes overlap the math
       const uint64_t sl2x2 = f2_pack(sl2, sl2), negm2 = f2_pack(-m_used, -m_used);
       uint64_t sum4[4] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
-      constexpr int KPC = 16 / EB;  // keys per 16-byte chunk of the P row
+      constexpr int KPC = 16 / PEB;  // keys per 16-byte chunk of the P row
 #pragma unroll
       for (int ch = 0; ch < A128_BN / KPC; ++ch) {
         float pf[KPC];
@@ -450,12 +531,8 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         }
         uint32_t pk[4];
 #pragma unroll
-        for (int w = 0; w < 4; ++w) {
-          if constexpr (FP8)
-            pk[w] = pack_e4m3x4(pf[4 * w], pf[4 * w + 1], pf[4 * w + 2], pf[4 * w + 3]);
-          else
-            pk[w] = BF16 ? pack_bf16(pf[2 * w], pf[2 * w + 1]) : pack_f16(pf[2 * w], pf[2 * w + 1]);
-        }
+        for (int w = 0; w < 4; ++w)
+          pk[w] = (BF16 && !FP8) ? pack_bf16(pf[2 * w], pf[2 * w + 1]) : pack_f16(pf[2 * w], pf[2 * w + 1]);
         // 16-byte chunk ch = keys [KPC ch, KPC (ch+1)): panel ch/8, swizzled position (ch%8) ^ (row%8)
         const uint32_t addr = p_row + (ch / 8) * PANEL + ((static_cast<uint32_t>(ch & 7) ^ swz) << 4);
         st_shared_v4(addr, pk[0], pk[1], pk[2], pk[3]);

@@ -501,8 +501,10 @@ ws_status launch_attn_fp8(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t 
   p.mx = d.MX;
   p.o = d.O;
   p.trace = trace;
-  const uint32_t kvb = A128_BN * DH;  // one e4m3 K or V block
-  const uint32_t base = 2 * A128_BM * DH + 2 * A128_BM * A128_BN + (2 * A128_MAX_STAGES + 16) * 8 + 16 + 1024;
+  const uint32_t kvb = A128_BN * DH;  // one e4m3 K block
+  // Q0 | Q1 (e4m3) | P0 | P1 (f16) | K ring | two f16 V buffers (e4m3 V lands in their upper
+  // halves) | barriers (+1 KB alignment slack)
+  const uint32_t base = 2 * A128_BM * DH + 2 * A128_BM * A128_BN * 2 + 2 * A128_BN * DH * 2 + APS_BAR_BYTES + 1024;
   int max_stages = (SMEM_LIMIT - (int)base) / (int)kvb;
   if (max_stages > A128_MAX_STAGES) max_stages = A128_MAX_STAGES;
   p.kv_stages = d.D > 0 ? d.D : max_stages;

@@ -174,10 +174,7 @@ def test_odd_query_tile_count_fp8(ws, dev, causal):
     q, k, v = (t.to(E4M3) for t in _inputs(B, H, S, Dh, BF16, dev))
     o, lse = ws.attn_fwd(q, k, v, causal=causal)
     torch.cuda.synchronize()
-    ro, rl = oracle.flash(as_f64(q), as_f64(k), as_f64(v), causal, block=128)
-    vmax = float(np.abs(as_f64(v)).max())
-    assert float(np.abs(as_f64(o) - ro).max()) <= 2.0 ** -4 * vmax
-    assert float(np.abs(as_f64(lse) - rl).max()) <= 1e-3
+    _check(q, k, v, o, lse, causal, tol_o=5e-2)
 
 
 E4M3 = torch.float8_e4m3fn
@@ -188,11 +185,9 @@ E4M3 = torch.float8_e4m3fn
 @pytest.mark.parametrize("S", [512, 2048])
 def test_fp8_e4m3_parity(ws, dev, causal, qk_div, S):
     """FP8 attention (ref PAPER.md:488): e4m3 q/k/v with per-tensor descales (powers of two keep the
-    reference's k/4 payloads exact in e4m3), P quantized to e4m3 for the P.V product.
-    Bars: LSE within 1e-3 (row sums accumulate the unquantized P in fp32); O within the e4m3 rounding
-    bound of P: each P carries a relative error <= 2^-4, so |O - O_ref| <= 2^-4 * max|V| per element
-    (sum_k |P_q - P| |v| / l <= 2^-4 max|v|). Norm-wise (max|dO| / max|O_ref|) it stays under 1e-1; it
-    is largest for flat softmax rows (qk_div = 4), whose outputs are small averages."""
+    reference's k/4 payloads exact in e4m3); QK^T in kind::f8f6f4, P in f16 against V converted to
+    f16 (exact). North-star bars: O max|d|/max|ref| <= 5e-2 and LSE within 1e-3; flat softmax rows
+    (qk_div = 4), whose outputs are small averages, are the hard case for the norm-wise bar."""
     q, k, v = _inputs(2, 2, S, 128, torch.float32, dev, qk_div=qk_div)
     sq, sk, sv = 0.5, 0.25, 2.0
     q8, k8, v8 = (q / sq).to(E4M3), (k / sk).to(E4M3), (v / sv).to(E4M3)
@@ -203,22 +198,28 @@ def test_fp8_e4m3_parity(ws, dev, causal, qk_div, S):
     ro, rl = oracle.flash(as_f64(q), as_f64(k), as_f64(v), causal)
     got_o, got_l = as_f64(o), as_f64(lse)
     assert np.abs(got_l - rl).max() <= 1e-3
-    assert np.abs(got_o - ro).max() <= float(v.abs().max()) / 16
-    assert rel_err(got_o, ro) <= 1e-1
+    assert rel_err(got_o, ro) <= 5e-2
+
+
+def test_fp8_kv_depth_over_smem_is_rejected(ws, dev):
+    """FP8 with f16 P and two f16 V buffers leaves room for 4 e4m3 K/V slots: D = 5 is SMEM_OVERFLOW."""
+    q = torch.zeros(1, 1, 256, 128, device=dev).to(E4M3)
+    with pytest.raises(ws.WsError) as e:
+        ws.attn_fwd(q, q, q, D=5)
+    assert e.value.code == "smem-overflow"
 
 
 def test_fp8_e4m3_rows_sum_to_one(ws, dev):
-    """V = 1: every O row is sum(P_e4m3) / l with l summed from the unquantized P, i.e. 1 within the
-    e4m3 rounding bound of P (relative error <= 2^-4 per element)."""
+    """V = 1: every O row is sum(P) / l with P in f16 and l summed in fp32: 1 within 1e-2."""
     q, k, _ = _inputs(1, 4, 2048, 128, torch.float32, dev, qk_div=1.0)
     v = torch.ones_like(q)
     for causal in (False, True):
         o, _ = ws.attn_fwd(q.to(E4M3), k.to(E4M3), v.to(E4M3), causal=causal)
         torch.cuda.synchronize()
-        assert (o.float() - 1).abs().max().item() <= 2.0 ** -4
+        assert (o.float() - 1).abs().max().item() <= 1e-2
 
 
-@pytest.mark.parametrize("D", [2, 3, 8])
+@pytest.mark.parametrize("D", [2, 3, 4])
 def test_fp8_e4m3_kv_aref_depths_and_shards(ws, dev, D):
     """FP8 path: every K/V ring depth gives the same result, and (b,h) shards tile the output."""
     B, H, S = 2, 3, 768
