@@ -120,6 +120,15 @@ typedef struct ws_attn_desc {
 ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream);
 ws_status ws_attn_fwd(const ws_attn_desc* desc, void* cuda_stream);
 
+/* Prepared GEMM launches for repeated calls on the same buffers (small GEMMs are host-bound):
+ * create validates and encodes everything ws_gemm_tn would (same status codes), launch is a single
+ * kernel launch on the given stream (capturable into a CUDA graph), destroy frees the host-side
+ * plan. A plan belongs to the device that was current at create. */
+typedef struct ws_gemm_plan ws_gemm_plan;
+ws_status ws_gemm_plan_create(const ws_gemm_desc* desc, ws_gemm_plan** plan);
+ws_status ws_gemm_plan_launch(ws_gemm_plan* plan, void* cuda_stream);
+void ws_gemm_plan_destroy(ws_gemm_plan* plan);
+
 /* ws_attn_fwd plus a device trace of CTA (0,0): `trace` is a device buffer of 3*256*8 uint64
  * %clock64 stamps — per KV step j, the MMA issuer (role 0) and the first softmax warp of each Q
  * tile (roles 1, 2) record when they start waiting, pass each mbarrier and finish each stage.

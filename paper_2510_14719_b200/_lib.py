@@ -83,6 +83,9 @@ class WatchdogInfo(ctypes.Structure):
 
 EXPORTS = {
     "ws_gemm_tn": (ctypes.c_int, [ctypes.POINTER(GemmDesc), ctypes.c_void_p]),
+    "ws_gemm_plan_create": (ctypes.c_int, [ctypes.POINTER(GemmDesc), ctypes.POINTER(ctypes.c_void_p)]),
+    "ws_gemm_plan_launch": (ctypes.c_int, [ctypes.c_void_p, ctypes.c_void_p]),
+    "ws_gemm_plan_destroy": (None, [ctypes.c_void_p]),
     "ws_attn_fwd": (ctypes.c_int, [ctypes.POINTER(AttnDesc), ctypes.c_void_p]),
     "ws_attn_fwd_traced": (ctypes.c_int, [ctypes.POINTER(AttnDesc), ctypes.c_void_p, ctypes.c_void_p]),
     "ws_debug_gemm_trace": (None, [ctypes.c_void_p]),

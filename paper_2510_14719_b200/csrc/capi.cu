@@ -17,6 +17,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
+#include <new>
 #include <unordered_map>
 #include <string>
 
@@ -228,13 +229,26 @@ const bool g_trace_global = getenv("WS_GEMM_TRACE_GLOBAL") != nullptr;
 unsigned long long* g_gemm_trace = nullptr;  // ws_debug_gemm_trace
 unsigned long long* g_gemm_clk = nullptr;    // ws_debug_gemm_clock
 
+}  // namespace
+
+// A prepared GEMM launch (ws_gemm_plan_create): kernel, tensor maps, parameters and grid, so a
+// repeated call is one cudaLaunchKernelEx (small GEMMs are host-bound).
+struct ws_gemm_plan {
+  CUtensorMap ta, tb, tc;
+  ws::GemmParams p;
+  const void* kern = nullptr;
+  int grid = 0, smem = 0, cg = 1, dev = 0;
+};
+
+namespace {
+
 template <int IN, int OUT, int BN, int CG>
-ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
+ws_status prepare_gemm(const ws_gemm_desc& d, ws_gemm_plan& pl) {
   using namespace ws;
   const int in_dt = d.in_dtype, out_dt = d.out_dtype;
   const int kbox = 128 / elem_bytes(in_dt);
 
-  GemmParams p;
+  GemmParams& p = pl.p;
   p.M = (int)d.M;
   p.N = (int)d.N;
   p.K = (int)d.K;
@@ -269,7 +283,7 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   p.debug_deadlock = g_debug_deadlock;
   p.trace_global = g_trace_global;
 
-  CUtensorMap ta, tb, tc;
+  CUtensorMap &ta = pl.ta, &tb = pl.tb, &tc = pl.tc;
   ws_status s;
   if ((s = make_tmap(&ta, d.A, in_dt, nbat * d.M, d.K, d.lda, GEMM_BM, kbox, CU_TENSOR_MAP_L2_PROMOTION_L2_256B)) !=
       WS_OK)
@@ -285,14 +299,22 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
   WS_CUDA_CHECK(allow_smem(reinterpret_cast<const void*>(kern), (int)L.total));
   const int tiles = (p.num_m_blocks / CG) * p.num_n_blocks * p.batch;
   const int units = num_sms() / CG;  // persistent: one CTA (pair) per SM (pair)
-  int grid = CG * (d.persistent ? (tiles < units ? tiles : units) : tiles);
+  pl.grid = CG * (d.persistent ? (tiles < units ? tiles : units) : tiles);
+  pl.kern = reinterpret_cast<const void*>(kern);
+  pl.smem = (int)L.total;
+  pl.cg = CG;
+  pl.dev = current_device();
+  return WS_OK;
+}
+
+ws_status launch_plan(ws_gemm_plan& pl, cudaStream_t stream) {
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(GEMM_THREADS);
-  cfg.dynamicSmemBytes = L.total;
+  cfg.gridDim = dim3(pl.grid);
+  cfg.blockDim = dim3(ws::GEMM_THREADS);
+  cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = stream;
   cudaLaunchAttribute attr[1];
-  if (CG == 2) {
+  if (pl.cg == 2) {
     attr[0].id = cudaLaunchAttributeClusterDimension;
     attr[0].val.clusterDim.x = 2;
     attr[0].val.clusterDim.y = 1;
@@ -300,41 +322,44 @@ ws_status launch_gemm(const ws_gemm_desc& d, cudaStream_t stream) {
     cfg.attrs = attr;
     cfg.numAttrs = 1;
   }
+  pl.p.trace = g_gemm_trace;
+  pl.p.clk = g_gemm_clk;
   apply_wait_hint();
-  WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, ta, tb, tc, p));
+  void* args[] = {&pl.ta, &pl.tb, &pl.tc, &pl.p};
+  WS_CUDA_CHECK(cudaLaunchKernelExC(&cfg, pl.kern, args));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return WS_OK;
 }
 
 template <int IN, int BN>
-ws_status dispatch_out(const ws_gemm_desc& d, cudaStream_t st) {
+ws_status dispatch_out(const ws_gemm_desc& d, ws_gemm_plan& st) {
   if constexpr (BN == 512) {
     // 256 x 512 pair tiles exist only as cta_group::2 (checked by the caller)
     switch (d.out_dtype) {
-      case WS_F32: return launch_gemm<IN, ws::OUT_F32, BN, 2>(d, st);
-      case WS_BF16: return launch_gemm<IN, ws::OUT_BF16, BN, 2>(d, st);
-      case WS_F16: return launch_gemm<IN, ws::OUT_F16, BN, 2>(d, st);
+      case WS_F32: return prepare_gemm<IN, ws::OUT_F32, BN, 2>(d, st);
+      case WS_BF16: return prepare_gemm<IN, ws::OUT_BF16, BN, 2>(d, st);
+      case WS_F16: return prepare_gemm<IN, ws::OUT_F16, BN, 2>(d, st);
     }
     return fail(WS_TYPE, "out_dtype must be F32, BF16 or F16");
   }
   if (d.cta_pair) {
     switch (d.out_dtype) {
-      case WS_F32: return launch_gemm<IN, ws::OUT_F32, BN, 2>(d, st);
-      case WS_BF16: return launch_gemm<IN, ws::OUT_BF16, BN, 2>(d, st);
-      case WS_F16: return launch_gemm<IN, ws::OUT_F16, BN, 2>(d, st);
+      case WS_F32: return prepare_gemm<IN, ws::OUT_F32, BN, 2>(d, st);
+      case WS_BF16: return prepare_gemm<IN, ws::OUT_BF16, BN, 2>(d, st);
+      case WS_F16: return prepare_gemm<IN, ws::OUT_F16, BN, 2>(d, st);
     }
   } else {
     switch (d.out_dtype) {
-      case WS_F32: return launch_gemm<IN, ws::OUT_F32, BN, 1>(d, st);
-      case WS_BF16: return launch_gemm<IN, ws::OUT_BF16, BN, 1>(d, st);
-      case WS_F16: return launch_gemm<IN, ws::OUT_F16, BN, 1>(d, st);
+      case WS_F32: return prepare_gemm<IN, ws::OUT_F32, BN, 1>(d, st);
+      case WS_BF16: return prepare_gemm<IN, ws::OUT_BF16, BN, 1>(d, st);
+      case WS_F16: return prepare_gemm<IN, ws::OUT_F16, BN, 1>(d, st);
     }
   }
   return fail(WS_TYPE, "out_dtype must be F32, BF16 or F16");
 }
 
 template <int BN>
-ws_status dispatch_in(const ws_gemm_desc& d, cudaStream_t st) {
+ws_status dispatch_in(const ws_gemm_desc& d, ws_gemm_plan& st) {
   switch (d.in_dtype) {
     case WS_F16: return dispatch_out<ws::IN_F16, BN>(d, st);
     case WS_BF16: return dispatch_out<ws::IN_BF16, BN>(d, st);
@@ -632,8 +657,10 @@ int32_t ws_watchdog(ws_watchdog_info* out) {
   return 1;
 }
 
-ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
-  g_last_error.clear();
+}  // extern "C"
+
+namespace {
+ws_status build_plan(const ws_gemm_desc* desc, ws_gemm_plan& pl) {
   if (!desc) return fail(WS_TYPE, "null descriptor");
   const ws_gemm_desc& d = *desc;
   if (d.M <= 0 || d.N <= 0 || d.K <= 0) return fail(WS_TYPE, "M, N, K must be positive");
@@ -682,9 +709,44 @@ ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
   if (d.batch < 0) return fail(WS_TYPE, "batch must be >= 0 (0 or 1 = one product)");
   if (nbat * d.M >= (int64_t)1 << 31 || nbat * d.N >= (int64_t)1 << 31)
     return fail(WS_TYPE, "batch*M and batch*N must fit in int32");
-  cudaStream_t st = reinterpret_cast<cudaStream_t>(cuda_stream);
-  return bn == 512 ? dispatch_in<512>(d, st) : bn == 256 ? dispatch_in<256>(d, st) : dispatch_in<128>(d, st);
+  return bn == 512 ? dispatch_in<512>(d, pl) : bn == 256 ? dispatch_in<256>(d, pl) : dispatch_in<128>(d, pl);
 }
+}  // namespace
+
+extern "C" {
+
+ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream) {
+  g_last_error.clear();
+  ws_gemm_plan pl;
+  const ws_status s = build_plan(desc, pl);
+  if (s != WS_OK) return s;
+  return launch_plan(pl, reinterpret_cast<cudaStream_t>(cuda_stream));
+}
+
+ws_status ws_gemm_plan_create(const ws_gemm_desc* desc, ws_gemm_plan** out) {
+  g_last_error.clear();
+  if (!out) return fail(WS_TYPE, "null plan pointer");
+  *out = nullptr;
+  auto* pl = new (std::nothrow) ws_gemm_plan();
+  if (!pl) return fail(WS_CUDA_ERROR, "out of host memory");
+  const ws_status s = build_plan(desc, *pl);
+  if (s != WS_OK) {
+    delete pl;
+    return s;
+  }
+  *out = pl;
+  return WS_OK;
+}
+
+ws_status ws_gemm_plan_launch(ws_gemm_plan* plan, void* cuda_stream) {
+  if (!plan) return fail(WS_TYPE, "null plan");
+  if (current_device() != plan->dev) return fail(WS_TYPE, "plan was created for another device");
+  return launch_plan(*plan, reinterpret_cast<cudaStream_t>(cuda_stream));
+}
+
+void ws_gemm_plan_destroy(ws_gemm_plan* plan) { delete plan; }
+
+
 
 ws_status ws_attn_fwd(const ws_attn_desc* desc, void* cuda_stream) {
   g_last_error.clear();

@@ -33,7 +33,7 @@ def _stream_ptr(stream: Optional[torch.cuda.Stream], device: Optional[torch.devi
 
 
 _SMS: dict = {}
-_DESC_CACHE: dict = {}
+_PLAN_CACHE: dict = {}
 
 
 class _OnDevice:
@@ -108,12 +108,14 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
         raise _lib.WsError(2, f"out must be {list(shape)} with contiguous rows" +
                            (" and batches stacked along rows" if batched else ""))
     lda, ldb, ldc = a.stride(-2), b.stride(-2), out.stride(-2)
-    # descriptors are reused for repeated calls on the same buffers and knobs (host cost per call
-    # matters for small GEMMs; scripts/host_overhead.py)
+    # prepared launches (ws_gemm_plan_*) are reused for repeated calls on the same buffers and
+    # knobs: a repeat is one kernel launch (host cost per call matters for small GEMMs)
     key = (a.data_ptr(), b.data_ptr(), out.data_ptr(), M, N, K, lda, ldb, ldc, nbat,
-           a.dtype, out.dtype, scale_a, scale_b, D, P, persistent, cta_pair, bn, group_m)
-    d = _DESC_CACHE.get(key)
-    if d is None:
+           a.dtype, out.dtype, scale_a, scale_b, D, P, persistent, cta_pair, bn, group_m, a.device.index)
+    plan = _PLAN_CACHE.get(key)
+    if plan is None:
+        if b.device != a.device or out.device != a.device:
+            raise _lib.WsError(2, "a, b and out must be on the same CUDA device")
         d = _lib.GemmDesc()
         d.in_dtype = _DT[a.dtype]
         d.out_dtype = _DT[out.dtype]
@@ -125,15 +127,33 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
         d.scale_a, d.scale_b = scale_a, scale_b
         d.D, d.P = D, P
         d.persistent, d.cta_pair, d.bn, d.group_m = int(persistent), int(cta_pair), bn, group_m
-        if len(_DESC_CACHE) >= 64:
-            _DESC_CACHE.clear()
-        _DESC_CACHE[key] = d
-    if b.device != a.device or out.device != a.device:
-        raise _lib.WsError(2, "a, b and out must be on the same CUDA device")
-    lib = _lib.load()
-    with _OnDevice(a.device):
-        _lib.check(lib.ws_gemm_tn(ctypes.byref(d), _stream_ptr(stream, a.device)))
+        plan = _GemmPlanHandle(d, a.device)
+        if len(_PLAN_CACHE) >= 64:
+            _PLAN_CACHE.clear()  # handles free their plans when dropped
+        _PLAN_CACHE[key] = plan
+    plan.launch(stream)
     return out
+
+
+class _GemmPlanHandle:
+    """Owns one ws_gemm_plan (include/ws.h): created on `device`, freed with the handle."""
+    __slots__ = ("ptr", "device", "_lib")
+
+    def __init__(self, desc, device: torch.device):
+        self._lib = _lib.load()
+        self.device = device
+        self.ptr = ctypes.c_void_p()
+        with _OnDevice(device):
+            _lib.check(self._lib.ws_gemm_plan_create(ctypes.byref(desc), ctypes.byref(self.ptr)))
+
+    def launch(self, stream: Optional[torch.cuda.Stream] = None):
+        with _OnDevice(self.device):
+            _lib.check(self._lib.ws_gemm_plan_launch(self.ptr, _stream_ptr(stream, self.device)))
+
+    def __del__(self):
+        if getattr(self, "ptr", None) and self.ptr.value:
+            self._lib.ws_gemm_plan_destroy(self.ptr)
+            self.ptr = ctypes.c_void_p()
 
 
 def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool = False,
@@ -141,7 +161,7 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool 
              lse: Optional[torch.Tensor] = None, D: int = 0, bh_range: Optional[tuple] = None,
              stream: Optional[torch.cuda.Stream] = None, trace: Optional[torch.Tensor] = None,
              kv_block: int = 0, scale_q: float = 1.0, scale_k: float = 1.0, scale_v: float = 1.0,
-             mx: Optional[torch.Tensor] = None):
+             mx: Optional[torch.Tensor] = None, persistent: bool = True):
     """FlashAttention forward over [B, H, S, Dh] tensors. Returns (o, lse) with lse fp32 [B, H, S]
     in natural-log units (lse = m + log l of the .k's running max m and row sum l).
 
@@ -149,7 +169,9 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool 
     (see ws_attn_fwd_traced in include/ws.h). kv_block: keys per K/V block (0 = auto = 128, or 64).
     float8_e4m3fn q/k/v (hdim 128): scale_q/k/v are the per-tensor descales; o is bf16.
     mx: optional fp32 [B, H, S] tensor receiving the exact row max m of the scaled scores (the
-    .k's %m): the .k's row sum is then l = exp(lse - mx) and its accumulator acc = o * l."""
+    .k's %m): the .k's row sum is then l = exp(lse - mx) and its accumulator acc = o * l.
+    persistent: False launches one CTA per work item instead of the persistent grid (RunSpec
+    persistent, ref driver.hpp:42-57)."""
     if q.device.type != "cuda":
         raise _lib.WsError(2, "operands must be CUDA tensors (no CPU path)")
     if not (q.dtype == k.dtype == v.dtype) or q.dtype not in (torch.float16, torch.bfloat16, torch.float8_e4m3fn):
@@ -186,6 +208,7 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool 
     d.Q, d.K, d.V, d.O = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr()
     d.LSE = lse.data_ptr()
     d.MX = mx.data_ptr() if mx is not None else None
+    d.grid_per_item = 0 if persistent else 1
     d.D = D
     lo, hi = bh_range if bh_range is not None else (0, B * H)
     d.bh_begin, d.bh_end = lo, hi

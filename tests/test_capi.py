@@ -17,7 +17,8 @@ def _declared_functions():
 
 
 def test_header_declares_the_path():
-    assert _declared_functions() == ["ws_attn_fwd", "ws_attn_fwd_traced", "ws_debug_gemm_clock", "ws_debug_gemm_trace", "ws_gemm_tn", "ws_last_error",
+    assert _declared_functions() == ["ws_attn_fwd", "ws_attn_fwd_traced", "ws_debug_gemm_clock", "ws_debug_gemm_trace", "ws_gemm_plan_create",
+                                    "ws_gemm_plan_destroy", "ws_gemm_plan_launch", "ws_gemm_tn", "ws_last_error",
                                     "ws_launch_count", "ws_run_kernel", "ws_run_kernel_spec", "ws_version",
                                     "ws_watchdog"]
 
@@ -96,6 +97,19 @@ def test_gemm_validation_codes(ws, kw, code):
     assert lib.ws_last_error()
 
 
+@pytest.mark.parametrize("kw,code", [(dict(D=2, P=3), "pipeline-infeasible"), (dict(M=200), "indivisible-tile"),
+                                     (dict(D=7), "smem-overflow"), (dict(in_dtype=0), "type")])
+def test_gemm_plan_validation_codes(ws, kw, code):
+    """A prepared launch validates exactly like ws_gemm_tn and hands out no plan on failure."""
+    lib = ws._lib.load()
+    plan = ctypes.c_void_p(0x1234)
+    st = lib.ws_gemm_plan_create(ctypes.byref(_gemm_desc(ws, **kw)), ctypes.byref(plan))
+    assert ws._lib.STATUS_NAMES[st] == code, lib.ws_last_error()
+    assert not plan.value
+    assert ws._lib.STATUS_NAMES[lib.ws_gemm_plan_launch(None, None)] == "type"
+    lib.ws_gemm_plan_destroy(None)
+
+
 def _attn_desc(ws, **kw):
     d = ws._lib.AttnDesc()
     d.dtype = ws._lib.WS_BF16
@@ -118,6 +132,7 @@ def _attn_desc(ws, **kw):
     (dict(dtype=0), "type"),                        # fp32 attention is not a tensor-core kind here
     (dict(dtype=3, Dh=64), "unsupported-kernel"),   # FP8 attention: hdim 128 only
     (dict(dtype=3, kv_block=64), "unsupported-kernel"),
+    (dict(dtype=3, D=5), "smem-overflow"),          # FP8: f16 P and V buffers leave room for 4 K slots
     (dict(bh_begin=1, bh_end=1), "type"),
 ])
 def test_attn_validation_codes(ws, kw, code):

@@ -282,3 +282,52 @@ def test_partial_last_wave_exact(ws, dev, M, N, K, out_dt, kw):
         assert np.array_equal(as_f64(got), want)
     else:
         assert torch.equal(got, torch.from_numpy(want).to(dev).to(out_dt))
+
+
+def test_prepared_launch_and_cuda_graph(ws, dev):
+    """Repeated calls go through a cached prepared launch (ws_gemm_plan_*) and capture into a CUDA
+    graph: replaying the graph gives the bit-exact result again (C1 shape, fp32 out)."""
+    a = ref_tensor("a", (1024, 1024), F16, dev)
+    b = ref_tensor("b", (1024, 1024), F16, dev)
+    c = torch.empty(1024, 1024, dtype=F32, device=dev)
+    want = _want(1024, 1024, 1024)
+    side = torch.cuda.Stream(dev)
+    side.wait_stream(torch.cuda.current_stream(dev))
+    g = torch.cuda.CUDAGraph()
+    with torch.cuda.stream(side):
+        ws.gemm_tn(a, b, c)
+        with torch.cuda.graph(g, stream=side):
+            for _ in range(3):
+                ws.gemm_tn(a, b, c)
+    torch.cuda.current_stream(dev).wait_stream(side)
+    c.zero_()
+    g.replay()
+    torch.cuda.synchronize()
+    assert np.array_equal(as_f64(c), want)
+    n0 = ws.launch_count()
+    for _ in range(5):
+        ws.gemm_tn(a, b, c)
+    torch.cuda.synchronize()
+    assert ws.launch_count() - n0 == 5
+    assert np.array_equal(as_f64(c), want)
+
+
+def test_plan_api_directly(ws, dev):
+    """ws_gemm_plan_create / launch / destroy through ctypes, as a C caller would use them."""
+    import ctypes
+
+    lib = ws._lib.load()
+    a = ref_tensor("a", (256, 512), BF16, dev)
+    b = ref_tensor("b", (256, 512), BF16, dev)
+    c = torch.empty(256, 256, dtype=F32, device=dev)
+    d = ws._lib.GemmDesc(in_dtype=ws._lib.WS_BF16, out_dtype=ws._lib.WS_F32, M=256, N=256, K=512,
+                         A=a.data_ptr(), lda=512, B=b.data_ptr(), ldb=512, C=c.data_ptr(), ldc=256,
+                         scale_a=1.0, scale_b=1.0, persistent=1)
+    plan = ctypes.c_void_p()
+    assert lib.ws_gemm_plan_create(ctypes.byref(d), ctypes.byref(plan)) == 0
+    s = torch.cuda.current_stream(dev).cuda_stream
+    for _ in range(2):
+        assert lib.ws_gemm_plan_launch(plan, s) == 0
+    torch.cuda.synchronize()
+    lib.ws_gemm_plan_destroy(plan)
+    assert np.array_equal(as_f64(c), _want(256, 256, 512))
