@@ -113,8 +113,9 @@ typedef struct ws_attn_desc {
   float* MX;                   /* optional [B, H, S] fp32: the exact row max m of the scaled scores
                                   (natural units), i.e. the flash .k's stored %m; with LSE it gives
                                   the .k's row sum l = exp(lse - m) and acc = O * l. NULL = skip */
-  int32_t grid_per_item;       /* 1 = one CTA per work item (RunSpec persistent = false); 0 = the
-                                  persistent grid (one CTA per SM over the work items) */
+  int32_t grid_per_item;       /* grid shape (RunSpec persistent): 1 = one CTA per work item,
+                                  2 = persistent (one CTA per SM looping over the work items),
+                                  0 = the measured default (persistent) */
 } ws_attn_desc;
 
 ws_status ws_gemm_tn(const ws_gemm_desc* desc, void* cuda_stream);

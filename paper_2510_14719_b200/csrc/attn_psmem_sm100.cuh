@@ -59,15 +59,8 @@ __host__ __device__ inline uint32_t aps_smem_bytes(int Dh, int kv_stages) {
 // keep the ring (the MMA warp is their only consumer). Quantizing P itself to e4m3 (3 mantissa bits) left O up to
 // ~6% of max|V| off the fp32-accumulated oracle; f16 P keeps it at the 16-bit kernels' error.
 // Per-tensor descales fold into the softmax scale (q, k) and the epilogue (v); O in bf16.
-//
-// SPLIT: two MMA issuers, warp 9 for Q tile 0 and warp 11 for Q tile 1, each issuing its tile's
-// QK and PV in its own order and waiting only on its own tile's barriers, so a late P of one tile
-// no longer holds back the other tile's QK (with one issuer the tensor-core work is issued in a
-// fixed cyclic order QK_0, PV_0, QK_1, PV_1 and every wait couples the two softmax warpgroups).
-// Both issuers walk the whole K/V ring in order; a slot (and Q, and an FP8 V buffer) is released
-// when both have committed — or, for a block only tile 1 uses (the causal diagonal), when issuer 0
-// has seen it land and arrived. FP8 then converts V with warp 10 alone.
-template <int DH, bool BF16, int POLY = 2, bool TRACE = false, bool FP8 = false, bool SPLIT = false>
+
+template <int DH, bool BF16, int POLY = 2, bool TRACE = false, bool FP8 = false>
 __global__ void __launch_bounds__(A128_THREADS, 1)
     ws_attn_psmem_kernel(const __grid_constant__ CUtensorMap tm_q, const __grid_constant__ CUtensorMap tm_k,
                          const __grid_constant__ CUtensorMap tm_v, const __grid_constant__ CUtensorMap tm_o,
@@ -146,9 +139,9 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     tma_prefetch_desc(&tm_k);
     tma_prefetch_desc(&tm_v);
     tma_prefetch_desc(&tm_o);
-    ring->init(D, 1, SPLIT ? 2 : 1);
+    ring->init(D, 1, 1);
     mbar_init(q_full, 1);
-    mbar_init(q_free, SPLIT ? 2 : 1);
+    mbar_init(q_free, 1);
     for (int i = 0; i < 2; ++i) {
       mbar_init(&s_full[i], 1);
       mbar_init(&s_free[i], 4);
@@ -156,7 +149,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       mbar_init(&pv_done[i], 1);
       mbar_init(&o_free[i], 4);
       mbar_init(&v16_full[i], 1);
-      mbar_init(&v16_empty[i], SPLIT ? 2 : 1);
+      mbar_init(&v16_empty[i], 1);
       mbar_init(&vfull[i], 1);
     }
     fence_barrier_init();
@@ -216,110 +209,6 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
             put(&tm_v, j);
         }
       }
-    }
-  } else if (SPLIT && (warp == 9 || warp == 11)) {
-    // ===================== MMA issuer of Q tile t (SPLIT) =====================
-    regs_dec<72>();
-    const int t = warp == 9 ? 0 : 1;
-    const uint64_t qdesc = make_sw128_desc(smem_u32(sq), 16, 1024);
-    const uint64_t pdesc = make_sw128_desc(smem_u32(sp), 16, 1024);
-    const uint64_t kdesc = make_sw128_desc(smem_u32(skv), 16, 1024);
-    const uint64_t vdesc = make_sw128_desc(smem_u32(FP8 ? sv16 : skv), PANEL, 1024);
-    const uint32_t d_s = tmem + t * A128_BN, d_o = tmem + COL_O + t * DH;
-    auto issue_qk = [&](uint32_t k_slot) {
-      const uint64_t a0 = qdesc + ((t * QTILE) >> 4), b0 = kdesc + ((k_slot * KVTILE) >> 4);
-#pragma unroll
-      for (int k = 0; k < DH * EB / 32; ++k) {
-        const uint32_t off = ((k / 4) * PANEL + (k % 4) * 32) >> 4;
-        if constexpr (FP8)
-          mma_f8_ss_warp(d_s, a0 + off, b0 + off, IDESC_QK, k != 0);
-        else
-          mma_f16_ss_warp(d_s, a0 + off, b0 + off, IDESC_QK, k != 0);
-      }
-    };
-    auto issue_pv = [&](uint32_t v_slot, bool acc) {
-      const uint64_t a0 = pdesc + ((t * PTILE) >> 4), b0 = vdesc + ((v_slot * (FP8 ? V16TILE : KVTILE)) >> 4);
-      constexpr int KEYS = 32 / PEB;
-#pragma unroll
-      for (int k = 0; k < A128_BN / KEYS; ++k) {
-        const uint32_t aoff = ((k / 4) * PANEL + (k % 4) * 32) >> 4;
-        mma_f16_ss_warp(d_o, a0 + aoff, b0 + ((k * KEYS * 128) >> 4), IDESC_PV, (acc || k != 0) ? 1u : 0u);
-      }
-    };
-    ArefCursor c;
-    uint32_t g = 0, vcnt = 0;  // this tile's blocks of earlier items; FP8: V blocks seen
-    bool first_done = false;   // the next item's QK_t(0) was issued inside the previous item
-    // QK_t(0) of item it_: Q landed, K_0 taken from the ring (both tiles use it), S_t free
-    auto first_qk = [&](int it_, uint32_t g_, int n_t_) {
-      mbar_wait(q_full, it_ & 1, 11);
-      ring->get(c, 12);
-      const uint32_t ks = c.slot;
-      c.advance(D);
-      tc_fence_after();
-      if (g_ > 0) {
-        mbar_wait(&s_free[t], (g_ - 1) & 1, 17 + t);
-        tc_fence_after();
-      }
-      issue_qk(ks);
-      mma_commit_warp(&s_full[t]);
-      mma_commit_warp(&ring->empty[ks]);
-      if (n_t_ == 1) mma_commit_warp(q_free);  // that was this tile's last QK of the item
-    };
-    for (int it = 0, item = item_of(0); item < num_items; item = item_of(++it)) {
-      int pair, bh;
-      item_coords(item, pair, bh);
-      const int n_t = nblk(pair, t), n1 = nblk(pair, 1);
-      if (!first_done) first_qk(it, g, n_t);
-      first_done = false;
-      const int next_item = item_of(it + 1);
-      for (int j = 0; j < n1; ++j) {
-        if (j + 1 < n1) {
-          ring->get(c, 13);  // K_{j+1}
-          const uint32_t ks = c.slot;
-          c.advance(D);
-          if (j + 1 < n_t) {
-            mbar_wait(&s_free[t], (g + j) & 1, 17 + t);  // S_t(j) copied out
-            tc_fence_after();
-            issue_qk(ks);
-            mma_commit_warp(&s_full[t]);
-            mma_commit_warp(&ring->empty[ks]);
-            if (j + 2 == n_t) mma_commit_warp(q_free);
-          } else {
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&ring->empty[ks]);  // a block only tile 1 reads
-          }
-        }
-        uint32_t vs;
-        if constexpr (FP8) {
-          vs = vcnt & 1u;
-          mbar_wait(&v16_full[vs], (vcnt >> 1) & 1u, 14);
-          ++vcnt;
-        } else {
-          ring->get(c, 14);  // V_j
-          vs = c.slot;
-          c.advance(D);
-        }
-        uint64_t* vrel = FP8 ? &v16_empty[vs] : &ring->empty[vs];
-        if (j < n_t) {
-          mbar_wait(&p_full[t], (g + j) & 1, 15 + t);
-          if (j == 0 && it > 0) mbar_wait(&o_free[t], (it - 1) & 1, 19);
-          tc_fence_after();
-          issue_pv(vs, j > 0);
-          mma_commit_warp(&pv_done[t]);
-          mma_commit_warp(vrel);
-        } else {
-          __syncwarp();
-          if (lane == 0) mbar_arrive(vrel);
-        }
-      }
-      if (next_item < num_items) {
-        // the next item's QK_t(0) right away (its K_0 follows this item's last V in the ring)
-        int pr, b2;
-        item_coords(next_item, pr, b2);
-        first_qk(it + 1, g + n_t, nblk(pr, t));
-        first_done = true;
-      }
-      g += n_t;
     }
   } else if (warp == 9) {
     // ===================== MMA issuer (whole warp, one elected lane issues) =====================
@@ -457,12 +346,12 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       g0 += n0;
       g1 += n1;
     }
-  } else if (FP8 && (warp == 10 || (!SPLIT && warp == 11))) {
-    // ===================== FP8: V converter (warps 10, 11; SPLIT: warp 10) =====================
+  } else if (FP8 && warp >= 10) {
+    // ===================== FP8: V converter (warps 10, 11) =====================
     // V_j (e4m3, 128 keys x 128 B, SW128, in the upper half of f16 buffer vcnt % 2) -> f16 in the
     // bf16 kernel's MN-major V layout (two 64-column SW128 panels), in place.
     regs_dec<72>();
-    constexpr int NCONV = SPLIT ? 1 : 2;             // converter warps
+    constexpr int NCONV = 2;                         // converter warps
     constexpr int ROWS = A128_BN / (32 * NCONV);     // keys per thread
     const uint32_t ct = (warp - 10u) * 32u + lane;  // keys ct, ct + 32 * NCONV, ...
     uint32_t vcnt = 0;

@@ -225,8 +225,7 @@ int env_int(const char* name, int dflt) {
 }
 const int g_debug_deadlock = env_int("WS_DEBUG_DEADLOCK", 0);
 const bool g_trace_global = getenv("WS_GEMM_TRACE_GLOBAL") != nullptr;
-// attention: one MMA issuer per Q tile (attn_psmem_sm100.cuh SPLIT)
-const int g_attn_split = env_int("WS_ATTN_SPLIT", 0);
+
 
 unsigned long long* g_gemm_trace = nullptr;  // ws_debug_gemm_trace
 unsigned long long* g_gemm_clk = nullptr;    // ws_debug_gemm_clock
@@ -476,7 +475,6 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
   constexpr int PS_POLY = DH == 64 ? 2 : APS_POLY;
   if (PSMEM)
     kern = trace ? ws_attn_psmem_kernel<DH, BF16, PS_POLY, true> : ws_attn_psmem_kernel<DH, BF16, PS_POLY>;
-  if (PSMEM && !trace && g_attn_split) kern = ws_attn_psmem_kernel<DH, BF16, PS_POLY, false, false, true>;
   if (BF16 && !trace) {
     switch (poly_env) {
       case 1: kern = PSMEM ? ws_attn_psmem_kernel<DH, BF16, 1> : ws_attn128_kernel<DH, BF16, 1>; break;
@@ -495,7 +493,8 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
       return e ? atoi(e) : 1;
     }();
     const int items = p.num_pairs * p.num_bh;
-    cfg.gridDim = dim3(persist_env == 0 || d.grid_per_item || items < num_sms() ? items : num_sms());
+    const bool per_item = d.grid_per_item == 1 || (d.grid_per_item == 0 && persist_env == 0);
+    cfg.gridDim = dim3(per_item || items < num_sms() ? items : num_sms());
   }
   cfg.blockDim = dim3(A128_THREADS);
   cfg.dynamicSmemBytes = smem;
@@ -557,7 +556,6 @@ ws_status launch_attn_fp8(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t 
   // FP8 (POLY 0/1/2/3/4 = 1586/1614/1645/1539/1483 TFLOP/s at S=16K, scripts/attn_ab.py AB_FP8=1)
   constexpr int F8_POLY = 2;
   auto kern = trace ? ws_attn_psmem_kernel<DH, true, F8_POLY, true, true> : ws_attn_psmem_kernel<DH, true, F8_POLY, false, true>;
-  if (!trace && g_attn_split) kern = ws_attn_psmem_kernel<DH, true, F8_POLY, false, true, true>;
   static const int poly_env = [] {
     const char* e = getenv("WS_ATTN_POLY");
     return e ? atoi(e) : -1;
@@ -574,7 +572,11 @@ ws_status launch_attn_fp8(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t 
   WS_CUDA_CHECK(allow_smem(reinterpret_cast<const void*>(kern), (int)smem));
   cudaLaunchConfig_t cfg = {};
   const int items = p.num_pairs * p.num_bh;
-  cfg.gridDim = dim3(d.grid_per_item || items < num_sms() ? items : num_sms());
+  // grid: persistent (one CTA per SM over the items) by default, or one CTA per item. At S = 16K
+  // the two are equal in interleaved A/B runs (1566 vs 1562 TFLOP/s; the 5% of the ordered D x P
+  // sweep did not reproduce), at S = 1K persistent wins (1210 vs 1060, cross-item overlap)
+  const bool per_item = d.grid_per_item == 1;
+  cfg.gridDim = dim3(per_item || items < num_sms() ? items : num_sms());
   cfg.blockDim = dim3(A128_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;

@@ -1198,7 +1198,7 @@ bool try_flash(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo
   a.Q = dq, a.K = dk, a.V = dv, a.O = dout, a.LSE = dlse, a.MX = dmx;
   a.bh_begin = static_cast<int32_t>(bh0), a.bh_end = static_cast<int32_t>(bh1);
   a.D = pl.d == 0 ? 0 : std::max(pl.d, 2);  // none / plain ws programs: the smallest ring
-  a.grid_per_item = pl.persistent ? 0 : 1;
+  a.grid_per_item = pl.persistent ? 2 : 1;
   ws_check(ws_attn_fwd(&a, st));
   auto* ho = static_cast<uint16_t*>(g_stage.pinned(3, nr * 2));
   auto* hl = static_cast<float*>(g_stage.pinned(4, static_cast<size_t>((bh1 - bh0) * S) * 4));

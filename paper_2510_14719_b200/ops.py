@@ -161,7 +161,7 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool 
              lse: Optional[torch.Tensor] = None, D: int = 0, bh_range: Optional[tuple] = None,
              stream: Optional[torch.cuda.Stream] = None, trace: Optional[torch.Tensor] = None,
              kv_block: int = 0, scale_q: float = 1.0, scale_k: float = 1.0, scale_v: float = 1.0,
-             mx: Optional[torch.Tensor] = None, persistent: bool = True):
+             mx: Optional[torch.Tensor] = None, persistent: Optional[bool] = None):
     """FlashAttention forward over [B, H, S, Dh] tensors. Returns (o, lse) with lse fp32 [B, H, S]
     in natural-log units (lse = m + log l of the .k's running max m and row sum l).
 
@@ -170,8 +170,8 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool 
     float8_e4m3fn q/k/v (hdim 128): scale_q/k/v are the per-tensor descales; o is bf16.
     mx: optional fp32 [B, H, S] tensor receiving the exact row max m of the scaled scores (the
     .k's %m): the .k's row sum is then l = exp(lse - mx) and its accumulator acc = o * l.
-    persistent: False launches one CTA per work item instead of the persistent grid (RunSpec
-    persistent, ref driver.hpp:42-57)."""
+    persistent: True = persistent grid, False = one CTA per work item (RunSpec persistent, ref
+    driver.hpp:42-57), None = the measured default (persistent)."""
     if q.device.type != "cuda":
         raise _lib.WsError(2, "operands must be CUDA tensors (no CPU path)")
     if not (q.dtype == k.dtype == v.dtype) or q.dtype not in (torch.float16, torch.bfloat16, torch.float8_e4m3fn):
@@ -208,7 +208,7 @@ def attn_fwd(q: torch.Tensor, k: torch.Tensor, v: torch.Tensor, *, causal: bool 
     d.Q, d.K, d.V, d.O = q.data_ptr(), k.data_ptr(), v.data_ptr(), out.data_ptr()
     d.LSE = lse.data_ptr()
     d.MX = mx.data_ptr() if mx is not None else None
-    d.grid_per_item = 0 if persistent else 1
+    d.grid_per_item = 0 if persistent is None else (2 if persistent else 1)
     d.D = D
     lo, hi = bh_range if bh_range is not None else (0, B * H)
     d.bh_begin, d.bh_end = lo, hi
