@@ -151,6 +151,8 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // programmatic dependent launch: the setup above overlapped the previous grid's tail
+  pdl_launch_dependents();
 
   if (warp == 8) {
     // ===================== producer: aref put =====================

@@ -158,6 +158,8 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  pdl_wait();  // programmatic dependent launch: the setup above overlapped the previous grid's tail
+  pdl_launch_dependents();
 
   // Register budget: the producer/MMA warpgroup needs few registers, the two softmax warpgroups
   // hold an S row each. 72*128 + 216*256 = 64512 <= 64K (= 168 * 384 at launch). Each role

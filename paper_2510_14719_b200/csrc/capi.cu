@@ -225,6 +225,10 @@ int env_int(const char* name, int dflt) {
 }
 const int g_debug_deadlock = env_int("WS_DEBUG_DEADLOCK", 0);
 const bool g_trace_global = getenv("WS_GEMM_TRACE_GLOBAL") != nullptr;
+// programmatic dependent launch of every kernel (WS_PDL=0 turns it off): a kernel's setup (barrier
+// init, TMEM alloc, descriptor prefetch) overlaps the previous grid's tail; measured +2-4% at short K
+// (scripts/pdl_ab.py), where it also puts the GEMM ahead of cuBLAS (which launches the same way)
+const int g_pdl = env_int("WS_PDL", 1);
 
 
 unsigned long long* g_gemm_trace = nullptr;  // ws_debug_gemm_trace
@@ -314,14 +318,19 @@ ws_status launch_plan(ws_gemm_plan& pl, cudaStream_t stream) {
   cfg.blockDim = dim3(ws::GEMM_THREADS);
   cfg.dynamicSmemBytes = pl.smem;
   cfg.stream = stream;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
+  cfg.attrs = attr;
   if (pl.cg == 2) {
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
+    attr[cfg.numAttrs].id = cudaLaunchAttributeClusterDimension;
+    attr[cfg.numAttrs].val.clusterDim.x = 2;
+    attr[cfg.numAttrs].val.clusterDim.y = 1;
+    attr[cfg.numAttrs].val.clusterDim.z = 1;
+    ++cfg.numAttrs;
+  }
+  if (g_pdl) {  // programmatic dependent launch: this grid's setup overlaps the previous one's tail
+    attr[cfg.numAttrs].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[cfg.numAttrs].val.programmaticStreamSerializationAllowed = 1;
+    ++cfg.numAttrs;
   }
   pl.p.trace = g_gemm_trace;
   pl.p.clk = g_gemm_clk;
@@ -412,6 +421,13 @@ ws_status launch_attn(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t stre
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   apply_wait_hint();
+  cudaLaunchAttribute pdl_attr[1];
+  if (g_pdl) {
+    pdl_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl_attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl_attr;
+    cfg.numAttrs = 1;
+  }
   WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, p));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return WS_OK;
@@ -500,6 +516,13 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   apply_wait_hint();
+  cudaLaunchAttribute pdl_attr[1];
+  if (g_pdl) {
+    pdl_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl_attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl_attr;
+    cfg.numAttrs = 1;
+  }
   WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, to, p));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return WS_OK;
@@ -581,6 +604,13 @@ ws_status launch_attn_fp8(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t 
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   apply_wait_hint();
+  cudaLaunchAttribute pdl_attr[1];
+  if (g_pdl) {
+    pdl_attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    pdl_attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = pdl_attr;
+    cfg.numAttrs = 1;
+  }
   WS_CUDA_CHECK(cudaLaunchKernelEx(&cfg, kern, tq, tk, tv, to, p));
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return WS_OK;

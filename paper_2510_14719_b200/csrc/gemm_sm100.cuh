@@ -168,6 +168,10 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     __syncthreads();
   tc_fence_after();
   const uint32_t tmem_base = *tmem_base_slot;
+  // setup above overlaps the previous grid's tail under programmatic dependent launch; global
+  // memory (operands, C) is touched only after it completed
+  pdl_wait();
+  pdl_launch_dependents();
   if (p.clk && blockIdx.x == 0 && threadIdx.x == 64) {
     p.clk[0] = clock64();
     p.clk[1] = globaltimer();

@@ -515,6 +515,12 @@ __device__ __forceinline__ uint64_t exp2_poly2(uint64_t x2) {
   return f2_pack(__uint_as_float(r0), __uint_as_float(r1));
 }
 
+// Programmatic dependent launch: wait until the preceding grid in the stream has completed and
+// its memory is visible (a no-op when the launch was not programmatic), and let the next grid's
+// CTAs be scheduled (its prologue then overlaps this grid's tail).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ uint4 ld_shared_v4(uint32_t addr) {
   uint4 v;
   asm volatile("ld.shared.v4.b32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr)
