@@ -296,6 +296,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
           ring->get(c, 13);  // K_{j+1}
           kslot = c.slot;
           c.advance(D);
+          if (lane == 0) WS_TRACE(0, g1 + j, 6);
           if (j + 1 < n0) {
             mbar_wait(&s_free[0], (g0 + j) & 1, 17);  // S_0(j) copied out
             tc_fence_after();
@@ -315,6 +316,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
           vslot = c.slot;
           c.advance(D);
         }
+        if (lane == 0) WS_TRACE(0, g1 + j, 7);
         if (j < n0) {
           mbar_wait(&p_full[0], (g0 + j) & 1, 15);  // C_0(j): P_0(j) in smem, O_0 rescaled
           if (j == 0 && it > 0) mbar_wait(&o_free[0], (it - 1) & 1, 19);  // previous O_0 copied out

@@ -12,7 +12,7 @@ __device__ __forceinline__ float fmax3_(float a, float b, float c) {
   return d;
 }
 
-template <int COLS, int POLY, bool XCHG, int NW, int ILP = 0>
+template <int COLS, int POLY, bool XCHG, int NW, int ILP = 0, bool NOSUM = false>
 __global__ void __launch_bounds__(128 * NW, 1) k(float* out, int steps) {
   __shared__ uint32_t tslot;
   __shared__ float xm[2][16][32];
@@ -86,7 +86,8 @@ __global__ void __launch_bounds__(128 * NW, 1) k(float* out, int steps) {
         uint64_t p2;
         if (attn_poly_pair(POLY, (c / 2) & 7)) p2 = exp2_poly2(x2);
         else { float x0, x1; f2_unpack(x2, x0, x1); p2 = f2_pack(ex2_approx(x0), ex2_approx(x1)); }
-        if (ILP) sc4[(c / 2) & 3] = f2_add(sc4[(c / 2) & 3], p2);
+        if (NOSUM) {}
+        else if (ILP) sc4[(c / 2) & 3] = f2_add(sc4[(c / 2) & 3], p2);
         else if ((c / 2) & 1) sb = f2_add(sb, p2); else sa = f2_add(sa, p2);
         float p0, p1; f2_unpack(p2, p0, p1);
         pk[(c - c0) / 2] = pack_bf16(p0, p1);
@@ -106,11 +107,11 @@ __global__ void __launch_bounds__(128 * NW, 1) k(float* out, int steps) {
   if (warp == 0) { tc_fence_after(); tmem_dealloc<1>(tslot, 512); }
 }
 
-template <int COLS, int POLY, bool XCHG, int NW, int ILP = 0>
+template <int COLS, int POLY, bool XCHG, int NW, int ILP = 0, bool NOSUM = false>
 void run1(float* o, const char* name) {
   const int steps = 2000, nw = NW;
-  k<COLS, POLY, XCHG, NW, ILP><<<148, 128 * nw>>>(o, steps);
-  k<COLS, POLY, XCHG, NW, ILP><<<148, 128 * nw>>>(o, steps);
+  k<COLS, POLY, XCHG, NW, ILP, NOSUM><<<148, 128 * nw>>>(o, steps);
+  k<COLS, POLY, XCHG, NW, ILP, NOSUM><<<148, 128 * nw>>>(o, steps);
   cudaError_t e = cudaDeviceSynchronize();
   float c = 0; cudaMemcpy(&c, o, 4, cudaMemcpyDeviceToHost);
   printf("%-28s warps/SMSP=%d cols=%3d: %7.1f cycles/step/warp, %6.1f cycles per SMSP per 128 cols %s\n", name, nw,
@@ -126,14 +127,13 @@ void run(float* o, int nw, const char* name) {
 
 int main() {
   float* o; cudaMalloc(&o, 64);
-  run1<128, 2, false, 1, 0>(o, "POLY=2 ILP0");
-  run1<128, 2, false, 1, 1>(o, "POLY=2 ILP1");
-  run1<128, 3, false, 1, 0>(o, "POLY=3 ILP0");
-  run1<128, 3, false, 1, 1>(o, "POLY=3 ILP1");
-  run1<128, 1, false, 1, 1>(o, "POLY=1 ILP1");
-  run1<128, 4, false, 1, 1>(o, "POLY=4 ILP1");
-  run1<128, 2, false, 2, 0>(o, "POLY=2 ILP0");
-  run1<128, 2, false, 2, 1>(o, "POLY=2 ILP1");
-  run1<128, 3, false, 2, 1>(o, "POLY=3 ILP1");
+  run1<128, 1, false, 2, 1>(o, "2w x128 POLY=1");
+  run1<128, 2, false, 2, 1>(o, "2w x128 POLY=2");
+  run1<128, 3, false, 2, 1>(o, "2w x128 POLY=3");
+  run1<128, 4, false, 2, 1>(o, "2w x128 POLY=4");
+  run1<128, 1, false, 2, 1, true>(o, "2w x128 POLY=1 nosum");
+  run1<128, 2, false, 2, 1, true>(o, "2w x128 POLY=2 nosum");
+  run1<128, 3, false, 2, 1, true>(o, "2w x128 POLY=3 nosum");
+  run1<128, 4, false, 2, 1, true>(o, "2w x128 POLY=4 nosum");
   return 0;
 }
