@@ -23,5 +23,12 @@ for causal in (False, True):
         ws.attn_fwd(q, k, v, causal=causal, kv_block=64)
     ws.attn_fwd(q[..., :64].contiguous(), k[..., :64].contiguous(), v[..., :64].contiguous(), causal=causal)
     ws.attn_fwd(q.to(torch.float8_e4m3fn), k.to(torch.float8_e4m3fn), v.to(torch.float8_e4m3fn), causal=causal)
+# persistent attention CTAs running more than one work item (256 items over 148 CTAs): the
+# cross-item hand-overs (q_free, o_free, first QK of the next item) and, for FP8, the V converter
+# warps' depth-2 ring across items
+qm = torch.randn(1, 64, 1024, 128, device=dev).bfloat16(); km = torch.randn_like(qm); vm = torch.randn_like(qm)
+for causal in (False, True):
+    ws.attn_fwd(qm, km, vm, causal=causal)
+    ws.attn_fwd(qm.to(torch.float8_e4m3fn), km.to(torch.float8_e4m3fn), vm.to(torch.float8_e4m3fn), causal=causal)
 torch.cuda.synchronize()
 print("sanitize workload done")
