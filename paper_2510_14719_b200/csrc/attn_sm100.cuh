@@ -318,11 +318,13 @@ __global__ void __launch_bounds__(ATTN_THREADS, 1)
         alpha = ex2_approx(m_used - m_blk);  // 0 on the first block (m_used = -inf)
         m_used = m_blk;
       }
+      // U_{j-1}[t] has landed (observed every step, so no pv_done phase completes unobserved —
+      // compute-sanitizer synccheck; it is long done by now). T_j completing implies U_{j-2}
+      // (issued before it) completed, and U_{j+1} cannot exist yet, so the buffer barrier of
+      // U_{j-1} is at most one phase behind and its parity test is unambiguous.
+      if (j > 0) mbar_wait(&pv_done[2 * t + ((j - 1) & 1)], ((j - 1) >> 1) & 1, 24 + t);
       if (j > 0 && __any_sync(0xffffffffu, need)) {
-        // correction: O_t row *= alpha once U_{j-1}[t] has landed. T_j completing implies U_{j-2}
-        // (issued before it) completed, and U_{j+1} cannot exist yet, so the buffer barrier of
-        // U_{j-1} is at most one phase behind and its parity test is unambiguous.
-        mbar_wait(&pv_done[2 * t + ((j - 1) & 1)], ((j - 1) >> 1) & 1, 24 + t);
+        // correction: O_t row *= alpha
         tc_fence_after();
         const uint64_t al2 = f2_pack(alpha, alpha);
 #pragma unroll 1
