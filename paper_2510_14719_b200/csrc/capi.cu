@@ -24,7 +24,6 @@
 #include "../../include/ws.h"
 #include "attn128_sm100.cuh"
 #include "attn_psmem_sm100.cuh"
-#include "attn_split_sm100.cuh"
 #include "attn_sm100.cuh"
 #include "gemm_sm100.cuh"
 
@@ -503,19 +502,6 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
       default: break;
     }
   }
-  // WS_ATTN_SPLIT (developer knob): the split-row softmax kernel (attn_split_sm100.cuh: 16 softmax
-  // warps, two threads per row) in place of the P-in-smem kernel it derives from
-  static const int split_env = [] {
-    const char* e = getenv("WS_ATTN_SPLIT");
-    return e ? atoi(e) : 0;
-  }();
-  const bool split = PSMEM && split_env > 0;
-  if (split) {
-    constexpr int SP_POLY = DH == 64 ? 2 : 1;
-    kern = trace ? ws_attn_split_kernel<DH, BF16, SP_POLY, true> : ws_attn_split_kernel<DH, BF16, SP_POLY>;
-    if (!trace && split_env == 2) kern = ws_attn_split_kernel<DH, BF16, 2>;
-    if (!trace && split_env == 3) kern = ws_attn_split_kernel<DH, BF16, 1>;
-  }
   WS_CUDA_CHECK(allow_smem(reinterpret_cast<const void*>(kern), (int)smem));
   cudaLaunchConfig_t cfg = {};
   {
@@ -529,7 +515,7 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
     const bool per_item = d.grid_per_item == 1 || (d.grid_per_item == 0 && persist_env == 0);
     cfg.gridDim = dim3(per_item || items < num_sms() ? items : num_sms());
   }
-  cfg.blockDim = dim3(split ? ASP_THREADS : A128_THREADS);
+  cfg.blockDim = dim3(A128_THREADS);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = stream;
   apply_wait_hint();
