@@ -7,6 +7,7 @@ import paper_2510_14719_b200 as ws
 ap = argparse.ArgumentParser()
 ap.add_argument("what", choices=["gemm", "gemm_fp8", "attn", "attn_causal", "attn_causal64", "attn_fp8"])
 ap.add_argument("--K", type=int, default=16384)
+ap.add_argument("--N", type=int, default=8192)  # gemm: an N-column shard (strong scaling) when < 8192
 ap.add_argument("--n", type=int, default=3)
 ap.add_argument("--bn", type=int, default=0)
 ap.add_argument("--D", type=int, default=0)
@@ -17,8 +18,8 @@ a = ap.parse_args()
 dev = torch.device("cuda")
 if a.what.startswith("gemm"):
     dt = torch.float8_e4m3fn if a.what == "gemm_fp8" else torch.bfloat16
-    A = torch.randn(8192, a.K, device=dev).to(dt); B = torch.randn(8192, a.K, device=dev).to(dt)
-    C = torch.empty(8192, 8192, device=dev, dtype=torch.bfloat16)
+    A = torch.randn(8192, a.K, device=dev).to(dt); B = torch.randn(a.N, a.K, device=dev).to(dt)
+    C = torch.empty(8192, a.N, device=dev, dtype=torch.bfloat16)
     for _ in range(a.n):
         ws.gemm_tn(A, B, C, bn=a.bn, D=a.D, P=a.P, cta_pair=a.cta_pair)
 else:
