@@ -826,22 +826,82 @@ void gemm_launch_knobs(ws_gemm_desc& d, const Plan& pl, int64_t Kp) {
 }
 
 bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo, int64_t hi, int dt, const Plan& pl,
+              cudaStream_t st);
+
+// Several independent dot chains in one loop (the reference's `twochain` test kernels,
+// ref proj/tests/support/kernel_gen.hpp:55-78: u += a.a^T, v += b.b^T, stored to c and d): each
+// chain — its loads, its dot, an optional relu of it, and the store of its accumulator — is cut
+// out into a single-chain kernel and run as one gemm. All chains are validated before any runs.
+bool try_gemm_chains(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo, int64_t hi, int dt,
+                     const Plan& pl, cudaStream_t st) {
+  std::vector<const Op*> dots;
+  for (const Op* o : tile_ops(g.body))
+    if (o->k == K::Dot) dots.push_back(o);
+  if (dots.size() < 2) return false;
+  std::vector<Kernel> parts;
+  std::set<const Op*> used_body, used_store;
+  for (const Op* d : dots) {
+    Kernel gk = g;
+    std::set<std::string> keep = {d->res, d->args[0], d->args[1]};
+    for (const Op& o : g.body)  // a relu of this chain's new accumulator belongs to it
+      if (o.k == K::Ew && o.fn == "relu" && o.args.size() == 1 && o.args[0] == d->res) keep.insert(o.res);
+    // iter args carrying this chain's values (acc, relu) and the epilogue values derived from them
+    std::set<std::string> carried;
+    const Op* y = yield_op(g);
+    if (!y) return false;
+    for (size_t i = 0; i < y->args.size() && i < g.iter.size(); ++i)
+      if (keep.count(y->args[i])) carried.insert(g.iter[i].first);
+    gk.body.clear();
+    for (const Op& o : g.body) {
+      const bool tile = o.k == K::Load || o.k == K::Dot || o.k == K::Ew || o.k == K::Reduce;
+      if (!tile || keep.count(o.res)) {
+        gk.body.push_back(o);
+        if (tile) used_body.insert(&o);
+      }
+    }
+    gk.epi.clear();
+    for (const Op& o : g.epi) {
+      if (o.k == K::Store) {
+        std::string v = o.args.empty() ? "" : o.args[0];
+        if (const Op* m = def_of(g.epi, v); m && m->k == K::Ew && m->fn == "mul") v = m->args[0];
+        if (!carried.count(v)) continue;
+        used_store.insert(&o);
+      } else if (o.k == K::Ew && o.fn == "mul" && !carried.count(o.args.empty() ? "" : o.args[0])) {
+        continue;
+      }
+      gk.epi.push_back(o);
+    }
+    // structure check only (an empty pid range runs nothing)
+    if (!try_gemm(gk, bufs, lo, lo, dt, pl, st)) return false;
+    parts.push_back(std::move(gk));
+  }
+  for (const Op* o : tile_ops(g.body))
+    if (o->k != K::ConstTile && !used_body.count(o)) return false;  // a tile op outside every chain
+  for (const Op& o : g.epi)
+    if (o.k == K::Store && !used_store.count(&o)) return false;
+  for (const Kernel& gk : parts)
+    if (!try_gemm(gk, bufs, lo, hi, dt, pl, st)) return false;
+  return true;
+}
+
+bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo, int64_t hi, int dt, const Plan& pl,
               cudaStream_t st) {
-  // body: exactly two loads and one dot(a, b.T, acc=<iter arg>), optional relu of the new acc,
-  // yield; prologue acc init = zeros; epilogue: store of the acc (or of the relu'd iter arg), or
-  // of `ew mul acc, <1x1 const>`
+  // body: the loads and one dot(a, b.T, acc=<iter arg>) (a and b may be one load: a Gram product),
+  // optional relu of the new acc, yield; prologue acc init = zeros; epilogue: store of the acc (or
+  // of the relu'd iter arg), or of `ew mul acc, <1x1 const>`
   const Op* dot = nullptr;
   std::vector<const Op*> loads;
   const Op* relu = nullptr;
   for (const Op* o : tile_ops(g.body)) {
     if (o->k == K::Load) loads.push_back(o);
     else if (o->k == K::Dot) {
-      if (dot) return false;
+      if (dot) return try_gemm_chains(g, bufs, lo, hi, dt, pl, st);
       dot = o;
     } else if (o->k == K::Ew && o->fn == "relu" && !relu) relu = o;
     else return false;
   }
-  if (!dot || loads.size() != 2 || !dot->trans) return false;
+  if (!dot || !dot->trans) return false;
+  if (loads.size() != 2 && !(loads.size() == 1 && dot->args[0] == dot->args[1])) return false;
   const Op* la = def_of(g.body, dot->args[0]);
   const Op* lb = def_of(g.body, dot->args[1]);
   if (!la || !lb || la->k != K::Load || lb->k != K::Load) return false;
