@@ -810,6 +810,34 @@ def bench_fp8_and_c1(ws, torch, dev, stream, args, world, max_over_ranks, barrie
         b = (torch.randn(n_hi - n_lo, K, device=dev) * 0.5).to(torch.float8_e4m3fn)
         ms = timed(lambda: ws.gemm_tn(a, b, c, scale_a=0.5, scale_b=2.0))
         res["c3_fp8_tflops_per_k"][str(K)] = round(gemm_flops(K) / (ms * 1e-3) / 1e12, 1)
+        if K in (2048, 16384) and world == 1 and not args.no_vs_cublas:
+            # context: cuBLASLt's FP8 GEMM (torch._scaled_mm, same e4m3 operands, per-tensor scales,
+            # bf16 out) in alternating windows on this box
+            try:
+                sa = torch.tensor(0.5, device=dev)
+                sb = torch.tensor(2.0, device=dev)
+                lib_fn = lambda: torch._scaled_mm(a, b.t(), scale_a=sa, scale_b=sb, out_dtype=torch.bfloat16)
+                ours_fn = lambda: ws.gemm_tn(a, b, c, scale_a=0.5, scale_b=2.0)
+                for _ in range(3):
+                    lib_fn()
+                ms_o, ms_l = [], []
+                for w in range(6):
+                    for fn, acc in (((ours_fn, ms_o), (lib_fn, ms_l)) if w % 2 == 0 else ((lib_fn, ms_l), (ours_fn, ms_o))):
+                        torch.cuda.synchronize()
+                        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                        e0.record(stream)
+                        for _ in range(10):
+                            fn()
+                        e1.record(stream)
+                        torch.cuda.synchronize()
+                        acc.append(e0.elapsed_time(e1) / 10)
+                med = lambda xs: sorted(xs)[len(xs) // 2]
+                res.setdefault("c3_vs_cublaslt_same_box", {})[f"e4m3_8192x8192x{K}"] = {
+                    "ours_tflops": round(gemm_flops(K) / (med(ms_o) * 1e-3) / 1e12, 1),
+                    "cublaslt_tflops": round(gemm_flops(K) / (med(ms_l) * 1e-3) / 1e12, 1),
+                    "windows": "6 alternating windows of 10 launches each, medians (torch._scaled_mm)"}
+            except Exception as e:  # noqa: BLE001 — context only
+                res.setdefault("c3_vs_cublaslt_same_box", {})[f"e4m3_8192x8192x{K}"] = {"unavailable": str(e)[:120]}
         del a, b
     a = torch.randn(1024, 1024, device=dev).half()
     b = torch.randn(1024, 1024, device=dev).half()
