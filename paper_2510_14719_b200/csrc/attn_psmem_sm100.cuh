@@ -215,6 +215,15 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
   } else if (warp == 9) {
     // ===================== MMA issuer (whole warp, one elected lane issues) =====================
     regs_dec<72>();
+    // shared-space barrier addresses, computed once: the loop then issues no generic -> shared
+    // conversions (each re-derived the 1 KB-aligned base from the shared window)
+    const uint32_t a_sfull[2] = {smem_u32_pinned(&s_full[0]), smem_u32_pinned(&s_full[1])};
+    const uint32_t a_sfree[2] = {smem_u32_pinned(&s_free[0]), smem_u32_pinned(&s_free[1])};
+    const uint32_t a_pfull[2] = {smem_u32_pinned(&p_full[0]), smem_u32_pinned(&p_full[1])};
+    const uint32_t a_pvdone[2] = {smem_u32_pinned(&pv_done[0]), smem_u32_pinned(&pv_done[1])};
+    const uint32_t a_ofree[2] = {smem_u32_pinned(&o_free[0]), smem_u32_pinned(&o_free[1])};
+    const uint32_t a_qfull = smem_u32_pinned(q_full), a_qfree = smem_u32_pinned(q_free);
+    const uint32_t a_v16full = smem_u32_pinned(&v16_full[0]), a_v16empty = smem_u32_pinned(&v16_empty[0]);
     const uint64_t qdesc = make_sw128_desc(smem_u32(sq), 16, 1024);
     const uint64_t pdesc = make_sw128_desc(smem_u32(sp), 16, 1024);
     const uint64_t kdesc = make_sw128_desc(smem_u32(skv), 16, 1024);
@@ -253,17 +262,17 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     // QK released it).
     uint32_t k0slot = 0;
     auto first_qk0 = [&](int it_, uint32_t g0_) {
-      mbar_wait(q_full, it_ & 1, 11);
+      mbar_wait(a_qfull, it_ & 1, 11);
       ring->get(c, 12);  // K_0
       k0slot = c.slot;
       c.advance(D);
       tc_fence_after();
       if (g0_ > 0) {
-        mbar_wait(&s_free[0], (g0_ - 1) & 1, 17);  // the previous item's last S_0 copied out
+        mbar_wait(a_sfree[0], (g0_ - 1) & 1, 17);  // the previous item's last S_0 copied out
         tc_fence_after();
       }
       issue_qk(0, k0slot);
-      mma_commit_warp(&s_full[0]);
+      mma_commit_warp(a_sfull[0]);
     };
     bool qk0_issued = false;
     for (int it = 0, item = item_of(0); item < num_items; item = item_of(++it)) {
@@ -273,11 +282,11 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       if (!qk0_issued) first_qk0(it, g0);
       qk0_issued = false;
       if (g1 > 0) {
-        mbar_wait(&s_free[1], (g1 - 1) & 1, 18);
+        mbar_wait(a_sfree[1], (g1 - 1) & 1, 18);
         tc_fence_after();
       }
       issue_qk(1, k0slot);
-      mma_commit_warp(&s_full[1]);
+      mma_commit_warp(a_sfull[1]);
       mma_commit_warp(&ring->empty[k0slot]);
       const int next_item = item_of(it + 1);
       for (int j = 0; j < n1; ++j) {
@@ -285,12 +294,12 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         const bool more = j + 1 < n1;
         uint32_t kslot = 0;
         auto qk1 = [&]() {
-          mbar_wait(&s_free[1], (g1 + j) & 1, 18);
+          mbar_wait(a_sfree[1], (g1 + j) & 1, 18);
           tc_fence_after();
           issue_qk(1, kslot);
-          mma_commit_warp(&s_full[1]);
+          mma_commit_warp(a_sfull[1]);
           mma_commit_warp(&ring->empty[kslot]);
-          if (j + 2 == n1) mma_commit_warp(q_free);  // that was the item's last QK: Q reusable
+          if (j + 2 == n1) mma_commit_warp(a_qfree);  // that was the item's last QK: Q reusable
         };
         if (more) {
           ring->get(c, 13);  // K_{j+1}
@@ -298,10 +307,10 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
           c.advance(D);
           if (lane == 0) WS_TRACE(0, g1 + j, 6);
           if (j + 1 < n0) {
-            mbar_wait(&s_free[0], (g0 + j) & 1, 17);  // S_0(j) copied out
+            mbar_wait(a_sfree[0], (g0 + j) & 1, 17);  // S_0(j) copied out
             tc_fence_after();
             issue_qk(0, kslot);
-            mma_commit_warp(&s_full[0]);
+            mma_commit_warp(a_sfull[0]);
           }
           if (lane == 0) WS_TRACE(0, g1 + j, 1);
           if (!p.stagger) qk1();
@@ -310,7 +319,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         uint32_t vslot;
         if constexpr (FP8) {
           vslot = vcnt & 1u;  // V_j's f16 copy (the ring carries K only)
-          mbar_wait(&v16_full[vslot], (vcnt >> 1) & 1u, 14);
+          mbar_wait(a_v16full + 8u * vslot, (vcnt >> 1) & 1u, 14);
         } else {
           ring->get(c, 14);  // V_j
           vslot = c.slot;
@@ -318,12 +327,12 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
         }
         if (lane == 0) WS_TRACE(0, g1 + j, 7);
         if (j < n0) {
-          mbar_wait(&p_full[0], (g0 + j) & 1, 15);  // C_0(j): P_0(j) in smem, O_0 rescaled
-          if (j == 0 && it > 0) mbar_wait(&o_free[0], (it - 1) & 1, 19);  // previous O_0 copied out
+          mbar_wait(a_pfull[0], (g0 + j) & 1, 15);  // C_0(j): P_0(j) in smem, O_0 rescaled
+          if (j == 0 && it > 0) mbar_wait(a_ofree[0], (it - 1) & 1, 19);  // previous O_0 copied out
           tc_fence_after();
           if (lane == 0) WS_TRACE(0, g1 + j, 3);
           issue_pv(0, vslot, j > 0);
-          mma_commit_warp(&pv_done[0]);
+          mma_commit_warp(a_pvdone[0]);
         }
         // stagger: QK_1(j+1) after PV_0(j), so tile 1's S lands half a step after tile 0's and the
         // two softmax warpgroups' latency-bound phases (row max) interleave with the other's
@@ -333,14 +342,14 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
           first_qk0(it + 1, g0 + n0);  // the next item's T_0(0), ahead of this item's last PV_1
           qk0_issued = true;
         }
-        mbar_wait(&p_full[1], (g1 + j) & 1, 16);
-        if (j == 0 && it > 0) mbar_wait(&o_free[1], (it - 1) & 1, 19);
+        mbar_wait(a_pfull[1], (g1 + j) & 1, 16);
+        if (j == 0 && it > 0) mbar_wait(a_ofree[1], (it - 1) & 1, 19);
         tc_fence_after();
         if (lane == 0) WS_TRACE(0, g1 + j, 4);
         issue_pv(1, vslot, j > 0);
-        mma_commit_warp(&pv_done[1]);
+        mma_commit_warp(a_pvdone[1]);
         if constexpr (FP8) {
-          mma_commit_warp(&v16_empty[vslot]);
+          mma_commit_warp(a_v16empty + 8u * vslot);
           ++vcnt;
         } else {
           mma_commit_warp(&ring->empty[vslot]);
@@ -358,6 +367,9 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     constexpr int NCONV = 2;                         // converter warps
     constexpr int ROWS = A128_BN / (32 * NCONV);     // keys per thread
     const uint32_t ct = (warp - 10u) * 32u + lane;  // keys ct, ct + 32 * NCONV, ...
+    // pinned shared-space addresses (vfull / v16_full are adjacent pairs, the f16 V buffers too)
+    const uint32_t a_vfull = smem_u32_pinned(&vfull[0]), a_v16full = smem_u32_pinned(&v16_full[0]);
+    const uint32_t a_sv16 = smem_u32_pinned(sv16);
     uint32_t vcnt = 0;
     for (int it = 0, item = item_of(0); item < num_items; item = item_of(++it)) {
       int pair, bh;
@@ -365,8 +377,8 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       const int n1 = nblk(pair, 1);
       for (int j = 0; j < n1; ++j) {
         const uint32_t b = vcnt & 1u;
-        mbar_wait(&vfull[b], (vcnt >> 1) & 1u, 30);  // V_j landed
-        const uint32_t dst = smem_u32(sv16 + b * V16TILE), src = dst + V16TILE / 2;
+        mbar_wait(a_vfull + 8u * b, (vcnt >> 1) & 1u, 30);  // V_j landed
+        const uint32_t dst = a_sv16 + b * V16TILE, src = dst + V16TILE / 2;
 #pragma unroll
         for (int rr = 0; rr < ROWS; ++rr) {
           const uint32_t r = ct + 32u * NCONV * rr, sw = r & 7u;
@@ -392,7 +404,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
           named_bar_sync(3, 64);
         else
           __syncwarp();
-        if (ct == 0) mbar_arrive(&v16_full[b]);
+        if (ct == 0) mbar_arrive(a_v16full + 8u * b);
         ++vcnt;
       }
     }
@@ -408,9 +420,14 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     const uint32_t t_s = tmem + t_lane + t * A128_BN;
     const uint32_t t_o = tmem + t_lane + COL_O + t * DH;
     // this thread's row of P_t: two 128-byte-swizzled panels (keys 0-63, 64-127)
-    const uint32_t p_row = smem_u32(sp + t * PTILE) + row * 128u;
+    uint32_t p_row = smem_u32(sp + t * PTILE) + row * 128u;
+    asm volatile("mov.b32 %0, %0;" : "+r"(p_row));  // pinned (see smem_u32_pinned)
     const uint32_t swz = static_cast<uint32_t>(row & 7);
     const float sl2 = p.scale_log2;
+    // shared-space barrier addresses of this tile, computed once (see the MMA warp)
+    const uint32_t a_sfull = smem_u32_pinned(&s_full[t]), a_sfree = smem_u32_pinned(&s_free[t]);
+    const uint32_t a_pfull = smem_u32_pinned(&p_full[t]), a_pvdone = smem_u32_pinned(&pv_done[t]);
+    const uint32_t a_ofree = smem_u32_pinned(&o_free[t]);
     const bool tr = lane == 0 && q == 0;
     uint32_t g = 0;  // blocks of this tile processed by earlier items
     for (int it = 0, item = item_of(0); item < num_items; item = item_of(++it)) {
@@ -427,7 +444,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     float l = 0.f;
     for (int j = 0; j < n_t; ++j) {
       if (tr) WS_TRACE(1 + t, g + j, 0);
-      mbar_wait(&s_full[t], (g + j) & 1, 20 + t);
+      mbar_wait(a_sfull, (g + j) & 1, 20 + t);
       if (tr) WS_TRACE(1 + t, g + j, 1);
       tc_fence_after();
       // S in two halves: the row max of the first 64 columns runs while the second half is loading
@@ -459,7 +476,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       // S_t(j) is in registers: release the TMEM columns so QK_t(j+1) can run during this softmax
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&s_free[t]);
+      if (lane == 0) mbar_arrive(a_sfree);
       if (tr) WS_TRACE(1 + t, g + j, 2);
       if (diag) {
 #pragma unroll
@@ -487,7 +504,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       if (j > 0 && __any_sync(0xffffffffu, need)) {
         // correction: O_t *= alpha once PV_t(j-1) has landed. PV_t(j) needs this warp's p_full,
         // so pv_done is at most one phase behind and the parity test is unambiguous.
-        mbar_wait(&pv_done[t], (g + j - 1) & 1, 24 + t);
+        mbar_wait(a_pvdone, (g + j - 1) & 1, 24 + t);
         tc_fence_after();
         const uint64_t al2 = f2_pack(alpha, alpha);
 #pragma unroll 1
@@ -510,7 +527,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       if (tr) WS_TRACE(1 + t, g + j, 3);
       // P_t's shared-memory tile is free once PV_t(j-1) has read it (long done by now: PV_t(j-1) was
       // issued when this warp finished block j-1)
-      if (g + j > 0) mbar_wait(&pv_done[t], (g + j - 1) & 1, 24 + t);
+      if (g + j > 0) mbar_wait(a_pvdone, (g + j - 1) & 1, 24 + t);
       if (j == 0 && it > 0) {
         // the previous item's O_t was staged through this P tile: its TMA store must have read it
         if (warp == 4u * t && lane == 0) tma_store_wait_read<0>();
@@ -557,13 +574,13 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       fence_proxy_async_smem();  // generic-proxy stores -> visible to the tensor core's reads
       tc_fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&p_full[t]);
+      if (lane == 0) mbar_arrive(a_pfull);
       if (tr) WS_TRACE(1 + t, g + j, 5);
     }
     // epilogue: O_t / l -> global, lse once the last PV_t has completed. O_t is copied to registers
     // first and released (o_free) so the next item's PV_t(0) can overwrite it while this finishes.
     g += n_t;
-    mbar_wait(&pv_done[t], (g - 1) & 1, 26 + t);
+    mbar_wait(a_pvdone, (g - 1) & 1, 26 + t);
     tc_fence_after();
     uint32_t ov[DH];
 #pragma unroll
@@ -571,7 +588,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     tmem_wait_ld();
     tc_fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&o_free[t]);
+    if (lane == 0) mbar_arrive(a_ofree);
     if (tr) WS_TRACE(1 + t, g - 1, 6);
     const float inv_l = p.o_scale / l;  // V's per-tensor descale (FP8) folded into 1 / l
     const size_t grow = static_cast<size_t>(q_row0 + t * A128_BM + row);
@@ -582,7 +599,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     // ~7000 cycles per work item (scripts/attn_trace_items.py).
     constexpr int OPANELS = DH / 64;                          // 64 output columns per panel
     constexpr int PPANELS = static_cast<int>(PTILE / PANEL);  // staging panels in the P tile
-    const uint32_t ptile = smem_u32(sp + t * PTILE);
+    const uint32_t ptile = smem_u32_pinned(sp + t * PTILE);
 #pragma unroll
     for (int c = 0; c < OPANELS; ++c) {
       const uint32_t buf = ptile + (c % PPANELS) * PANEL;

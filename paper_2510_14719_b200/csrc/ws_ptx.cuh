@@ -13,6 +13,14 @@ namespace ws {
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
 }
+// A shared-space address pinned in a register: ptxas otherwise rematerialises generic -> shared
+// conversions at every use inside hot loops (S2R of the shared window and CTA id, the 1 KB base
+// alignment, the ring offset: ~10 instructions and an S2R latency per barrier operation).
+__device__ __forceinline__ uint32_t smem_u32_pinned(const void* p) {
+  uint32_t a;
+  asm volatile("mov.b32 %0, %1;" : "=r"(a) : "r"(smem_u32(p)));
+  return a;
+}
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
 
@@ -65,6 +73,10 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
+// the same on a shared-space address computed once (hot loops: no generic -> shared conversion)
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
 
 // arrive on the barrier at the same smem offset in CTA `cta` of this cluster
 __device__ __forceinline__ void mbar_arrive_cluster(uint64_t* bar, uint32_t cta) {
@@ -109,6 +121,10 @@ static __device__ __forceinline__ void mbar_wait_slow(uint32_t bar, uint32_t par
 // rule of the reference (ref proj/include/warpspec/sim.hpp:86-92) is realised.
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity, uint32_t tag = 0) {
   uint32_t a = smem_u32(bar);
+  if (mbar_try_wait(a, parity)) return;
+  mbar_wait_slow(a, parity, tag);
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity, uint32_t tag = 0) {
   if (mbar_try_wait(a, parity)) return;
   mbar_wait_slow(a, parity, tag);
 }
@@ -305,12 +321,13 @@ __device__ __forceinline__ void mma_f16_ts_warp(uint32_t d_tmem, uint32_t a_tmem
       "@e tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
       "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate));
 }
-__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) {
+__device__ __forceinline__ void mma_commit_warp(uint32_t bar) {
   asm volatile(
       "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
-      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
       : "memory");
 }
+__device__ __forceinline__ void mma_commit_warp(uint64_t* bar) { mma_commit_warp(smem_u32(bar)); }
 
 // kind::f16 with A from tensor memory (P in the PV product of attention)
 __device__ __forceinline__ void mma_f16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
