@@ -224,6 +224,8 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     const uint32_t a_ofree[2] = {smem_u32_pinned(&o_free[0]), smem_u32_pinned(&o_free[1])};
     const uint32_t a_qfull = smem_u32_pinned(q_full), a_qfree = smem_u32_pinned(q_free);
     const uint32_t a_v16full = smem_u32_pinned(&v16_full[0]), a_v16empty = smem_u32_pinned(&v16_empty[0]);
+    const uint32_t a_rfull = smem_u32_pinned(&ring->full[0]), a_rempty = smem_u32_pinned(&ring->empty[0]);
+    auto ring_get = [&](const ArefCursor& cc, uint32_t tag) { mbar_wait(a_rfull + 8u * cc.slot, cc.phase, tag); };
     const uint64_t qdesc = make_sw128_desc(smem_u32(sq), 16, 1024);
     const uint64_t pdesc = make_sw128_desc(smem_u32(sp), 16, 1024);
     const uint64_t kdesc = make_sw128_desc(smem_u32(skv), 16, 1024);
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     uint32_t k0slot = 0;
     auto first_qk0 = [&](int it_, uint32_t g0_) {
       mbar_wait(a_qfull, it_ & 1, 11);
-      ring->get(c, 12);  // K_0
+      ring_get(c, 12);  // K_0
       k0slot = c.slot;
       c.advance(D);
       tc_fence_after();
@@ -287,7 +289,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       }
       issue_qk(1, k0slot);
       mma_commit_warp(a_sfull[1]);
-      mma_commit_warp(&ring->empty[k0slot]);
+      mma_commit_warp(a_rempty + 8u * k0slot);
       const int next_item = item_of(it + 1);
       for (int j = 0; j < n1; ++j) {
         if (lane == 0) WS_TRACE(0, g1 + j, 0);
@@ -298,11 +300,11 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
           tc_fence_after();
           issue_qk(1, kslot);
           mma_commit_warp(a_sfull[1]);
-          mma_commit_warp(&ring->empty[kslot]);
+          mma_commit_warp(a_rempty + 8u * kslot);
           if (j + 2 == n1) mma_commit_warp(a_qfree);  // that was the item's last QK: Q reusable
         };
         if (more) {
-          ring->get(c, 13);  // K_{j+1}
+          ring_get(c, 13);  // K_{j+1}
           kslot = c.slot;
           c.advance(D);
           if (lane == 0) WS_TRACE(0, g1 + j, 6);
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
           vslot = vcnt & 1u;  // V_j's f16 copy (the ring carries K only)
           mbar_wait(a_v16full + 8u * vslot, (vcnt >> 1) & 1u, 14);
         } else {
-          ring->get(c, 14);  // V_j
+          ring_get(c, 14);  // V_j
           vslot = c.slot;
           c.advance(D);
         }
@@ -352,7 +354,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
           mma_commit_warp(a_v16empty + 8u * vslot);
           ++vcnt;
         } else {
-          mma_commit_warp(&ring->empty[vslot]);
+          mma_commit_warp(a_rempty + 8u * vslot);
         }
         if (lane == 0) WS_TRACE(0, g1 + j, 5);
       }
@@ -536,7 +538,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       // P = 2^(s*sl2 - m), packed to 16-bit pairs and stored 8 keys (16 bytes) at a time into the
       // 128B-swizzled K-major P tile as it is produced, so the shared-memory writes overlap the math
       const uint64_t sl2x2 = f2_pack(sl2, sl2), negm2 = f2_pack(-m_used, -m_used);
-      uint64_t sum4[4] = {f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f), f2_pack(0.f, 0.f)};
+      uint64_t sum4[4];  // row-sum partials, seeded by the first chunk (no adds of zero)
       constexpr int KPC = 16 / PEB;  // keys per 16-byte chunk of the P row
 #pragma unroll
       for (int ch = 0; ch < A128_BN / KPC; ++ch) {
@@ -553,7 +555,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
             f2_unpack(x2, x0, x1);
             p2 = f2_pack(ex2_approx(x0), ex2_approx(x1));
           }
-          sum4[e & 3] = f2_add(sum4[e & 3], p2);
+          sum4[e & 3] = ch == 0 ? p2 : f2_add(sum4[e & 3], p2);
           f2_unpack(p2, pf[2 * e], pf[2 * e + 1]);
         }
         uint32_t pk[4];
