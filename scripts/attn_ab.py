@@ -15,6 +15,8 @@ fp8 = os.environ.get("AB_FP8") == "1"
 cases = [(1, 16384, 128, False), (1, 16384, 128, True), (16, 1024, 128, False), (1, 16384, 64, True), (1, 16384, 64, False)]
 if os.environ.get("AB_SHORT") == "1":  # the C4 short-sequence cases
     cases = [(16, 1024, 128, False), (8, 2048, 128, False), (4, 4096, 128, False)]
+if os.environ.get("AB_D64") == "1":  # the hdim-64 cases only
+    cases = [(1, 16384, 64, True), (1, 16384, 64, False)]
 for (B, S, Dh, causal) in (cases[:3] if fp8 else cases):
     q = torch.randn(B, 16, S, Dh, device="cuda", dtype=torch.bfloat16); k = torch.randn_like(q); v = torch.randn_like(q)
     o = torch.empty_like(q); lse = torch.empty(B, 16, S, device="cuda")
@@ -48,4 +50,6 @@ for r in range(rounds):
 for v, rs in allres.items():
     if not rs: continue
     keys = rs[0].keys()
-    print(f"{v:40s}", {k: max(r[k] for r in rs) for k in keys})
+    stat = os.environ.get("AB_STAT", "max")  # max (default) or median over rounds
+    agg = (lambda xs: sorted(xs)[len(xs) // 2]) if stat == "median" else max
+    print(f"{v:40s}", {k: agg([r[k] for r in rs]) for k in keys})
