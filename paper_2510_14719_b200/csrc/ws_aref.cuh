@@ -31,7 +31,7 @@ static __device__ WatchdogRecord ws_watchdog_record;
 // torn down the context, which is how ws_watchdog() reports the Deadlock verdict
 static __device__ WatchdogRecord* ws_watchdog_host;
 // suspend-time hint (ns) for blocked waits; 0 = the hardware default (set by the host launcher)
-static __device__ uint32_t ws_wait_hint_ns;
+static __constant__ uint32_t ws_wait_hint_ns;  // constant bank: a cached LDC, not an L2 round trip per wait
 
 // The watchdog's report, out of line and noreturn: no caller state survives a trap, so the call
 // costs the wait sites nothing (an inline version that could fall back into the wait loop slowed
@@ -72,8 +72,9 @@ static __device__ uint32_t ws_wait_hint_ns;
 static __device__ __forceinline__ void mbar_wait_slow(uint32_t bar, uint32_t parity, uint32_t tag) {
   uint64_t t0 = globaltimer();
   uint32_t spins = 0;
-  // volatile load: written only by the host (cudaMemcpyToSymbol), never folded to its initialiser
-  const uint32_t hint = *reinterpret_cast<volatile uint32_t*>(&ws_wait_hint_ns);
+  // written only by the host (cudaMemcpyToSymbol) before the launch; a constant-bank read (the
+  // volatile global load it replaces cost every slow-path wait an L2 round trip)
+  const uint32_t hint = ws_wait_hint_ns;
   while (!(hint ? mbar_try_wait_hint(bar, parity, hint) : mbar_try_wait(bar, parity))) {
     if (((++spins) & 1023u) == 0 && globaltimer() - t0 > WS_WATCHDOG_NS) ws_watchdog_fire(bar, parity, tag);
   }
