@@ -593,6 +593,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
     if (lane == 0) mbar_arrive(a_ofree);
     if (tr) WS_TRACE(1 + t, g - 1, 6);
     const float inv_l = p.o_scale / l;  // V's per-tensor descale (FP8) folded into 1 / l
+    const uint64_t inv_l2 = f2_pack(inv_l, inv_l);
     const size_t grow = static_cast<size_t>(q_row0 + t * A128_BM + row);
     // O_t leaves through TMA: each thread writes its row (16-bit, 128B-swizzled, 64 columns per
     // 16 KB panel) into this tile's P buffer — free, since its last PV has completed — and one
@@ -615,7 +616,8 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           const int col = c * 64 + k8 * 8 + 2 * e;
-          const float a = __uint_as_float(ov[col]) * inv_l, b = __uint_as_float(ov[col + 1]) * inv_l;
+          float a, b;  // packed FMUL2: one multiply per column pair
+          f2_unpack(f2_mul(f2_pack(__uint_as_float(ov[col]), __uint_as_float(ov[col + 1])), inv_l2), a, b);
           w[e] = (BF16 || FP8) ? pack_bf16(a, b) : pack_f16(a, b);
         }
         st_shared_v4(buf + row * 128u + ((static_cast<uint32_t>(k8) ^ swz) << 4), w[0], w[1], w[2], w[3]);
