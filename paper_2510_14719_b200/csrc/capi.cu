@@ -449,10 +449,9 @@ ws_status launch_attn128(const ws_attn_desc& d, int bh0, int bh1, cudaStream_t s
     const char* e = getenv("WS_ATTN_STAGGER");
     return e ? atoi(e) : -1;
   }();
-  // staggered tile issue: +3-4 % at hdim 128; at hdim 64 (softmax-bound, half the tensor work per
-  // step) issuing both tiles' QKs back to back is ~1.2 % faster at every ring depth
-  // (scripts/attn_d64_sweep.py, profiles/r02b_attn_experiments.md)
-  p.stagger = stagger_env >= 0 ? stagger_env : (DH == 64 ? 0 : 1);
+  // staggered tile issue: +3-4 % at hdim 128 and, since the barrier addresses are pinned (leaner
+  // softmax), +2 % at hdim 64 as well (8-round medians; profiles/r02b_attn_experiments.md)
+  p.stagger = stagger_env >= 0 ? stagger_env : 1;
   p.causal = d.causal;
   // causal: (b,h) fastest so every head's heaviest query pairs run first (longest-first);
   // non-causal: the query pairs of one (b,h) run together and share its K/V in L2
