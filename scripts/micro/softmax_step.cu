@@ -207,11 +207,26 @@ template <int COLS, int POLY, bool XCHG>
 void run(float* o, int nw, const char* name) {
   if (nw == 1) run1<COLS, POLY, XCHG, 1>(o, name);
   if (nw == 2) run1<COLS, POLY, XCHG, 2>(o, name);
+  if (nw == 3) run1<COLS, POLY, XCHG, 3>(o, name);
   if (nw == 4) run1<COLS, POLY, XCHG, 4>(o, name);
 }
 
-int main() {
+int main(int argc, char** argv) {
   float* o; cudaMalloc(&o, 64);
+  if (argc > 1) {  // warps-per-SMSP sweep at 128 columns (3 or 4 Q tiles per CTA instead of 2)
+    run1<128, 1, false, 1, 1>(o, "1w x128 POLY=1");
+    run1<128, 2, false, 1, 1>(o, "1w x128 POLY=2");
+    run1<128, 1, false, 2, 1>(o, "2w x128 POLY=1");
+    run1<128, 2, false, 2, 1>(o, "2w x128 POLY=2");
+    run1<128, 3, false, 2, 1>(o, "2w x128 POLY=3");
+    run1<128, 1, false, 3, 1>(o, "3w x128 POLY=1");
+    run1<128, 2, false, 3, 1>(o, "3w x128 POLY=2");
+    run1<128, 3, false, 3, 1>(o, "3w x128 POLY=3");
+    run1<128, 1, false, 4, 1>(o, "4w x128 POLY=1");
+    run1<128, 2, false, 4, 1>(o, "4w x128 POLY=2");
+    run1<128, 3, false, 4, 1>(o, "4w x128 POLY=3");
+    return 0;
+  }
   run1<128, 1, false, 2, 1>(o, "2w x128 POLY=1");
   run1<128, 2, false, 2, 1>(o, "2w x128 POLY=2");
   run1<128, 3, false, 2, 1>(o, "2w x128 POLY=3");
