@@ -64,6 +64,26 @@ def test_full_range_scores(ws, dev, causal, Dh, kv_block):
     _check(q, k, v, o, lse, causal)
 
 
+@pytest.mark.parametrize("rise", [0.03, 0.1, -0.03])
+@pytest.mark.parametrize("Dh", [64, 128])
+@pytest.mark.parametrize("causal", [False, True])
+def test_scores_rising_along_keys(ws, dev, causal, Dh, rise):
+    """Scores that rise (or fall) steadily with the key index: every 128-key block lifts the row max
+    by 128 * rise (log2 units), so the speculative softmax step (exponentials against the running
+    max, row max only when the P row sum reaches 2^8) takes all of its branches — sum below the
+    bound, sum above it without a rescale, and a rescale with P recomputed."""
+    q, k, v = _inputs(1, 2, 2048, Dh, BF16, dev)
+    sl2 = 1.4426950408889634 / Dh ** 0.5  # default softmax scale, log2 units
+    keys = torch.arange(2048, device=dev, dtype=torch.float32)
+    q = q.clone()
+    k = k.clone()
+    q[..., 0] = 1.0
+    k[..., 0] = (rise / sl2 * keys).to(BF16)
+    o, lse = ws.attn_fwd(q, k, v, causal=causal)
+    torch.cuda.synchronize()
+    _check(q, k, v, o, lse, causal)
+
+
 @pytest.mark.parametrize("kv_block,D", [(64, 2), (64, 3), (64, 4), (128, 2), (128, 3)])
 @pytest.mark.parametrize("Dh", [64, 128])
 def test_kv_aref_depths(ws, dev, D, kv_block, Dh):
