@@ -34,6 +34,7 @@ def _stream_ptr(stream: Optional[torch.cuda.Stream], device: Optional[torch.devi
 
 _SMS: dict = {}
 _PLAN_CACHE: dict = {}
+_FAST_PLANS: dict = {}  # repeat-call key (see gemm_tn) -> the same plan handles as _PLAN_CACHE
 
 
 class _OnDevice:
@@ -75,6 +76,19 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
     bn: 0 = auto (the library picks 256 x 512 pair tiles from 16 K blocks when they fill the GPU,
     else 256-wide tiles, or 128-wide single-CTA tiles for small problems).
     """
+    if out is not None:
+        # repeat call on buffers already validated and planned (same addresses, shapes, strides,
+        # dtypes and knobs): straight to the prepared launch. Device pointers are unique across
+        # devices (UVA), so the key also pins the device.
+        fkey = (a.data_ptr(), b.data_ptr(), out.data_ptr(), a.shape, b.shape, out.shape, a.stride(),
+                b.stride(), out.stride(), a.dtype, b.dtype, out.dtype, scale_a, scale_b, D, P, persistent,
+                cta_pair, bn, group_m)
+        plan = _FAST_PLANS.get(fkey)
+        if plan is not None:
+            plan.launch(stream)
+            return out
+    else:
+        fkey = None
     if a.device.type != "cuda" or b.device.type != "cuda":
         raise _lib.WsError(2, "operands must be CUDA tensors (no CPU path)")
     if a.dtype != b.dtype or a.dtype not in (torch.float16, torch.bfloat16, torch.float8_e4m3fn):
@@ -130,25 +144,37 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
         plan = _GemmPlanHandle(d, a.device)
         if len(_PLAN_CACHE) >= 64:
             _PLAN_CACHE.clear()  # handles free their plans when dropped
+            _FAST_PLANS.clear()
         _PLAN_CACHE[key] = plan
+    if fkey is not None:
+        _FAST_PLANS[fkey] = plan
     plan.launch(stream)
     return out
 
 
 class _GemmPlanHandle:
     """Owns one ws_gemm_plan (include/ws.h): created on `device`, freed with the handle."""
-    __slots__ = ("ptr", "device", "_lib")
+    __slots__ = ("ptr", "device", "idx", "_lib", "_launch")
 
     def __init__(self, desc, device: torch.device):
         self._lib = _lib.load()
         self.device = device
+        self.idx = device.index if device.index is not None else torch.cuda.current_device()
+        self._launch = self._lib.ws_gemm_plan_launch
         self.ptr = ctypes.c_void_p()
         with _OnDevice(device):
             _lib.check(self._lib.ws_gemm_plan_create(ctypes.byref(desc), ctypes.byref(self.ptr)))
 
     def launch(self, stream: Optional[torch.cuda.Stream] = None):
+        cur = torch._C._cuda_getDevice()
+        if cur == self.idx:  # the common case: one cheap device query, no context switch
+            s = stream.cuda_stream if stream is not None else torch._C._cuda_getCurrentRawStream(cur)
+            rc = self._launch(self.ptr, s)
+            if rc:
+                _lib.check(rc)
+            return
         with _OnDevice(self.device):
-            _lib.check(self._lib.ws_gemm_plan_launch(self.ptr, _stream_ptr(stream, self.device)))
+            _lib.check(self._launch(self.ptr, _stream_ptr(stream, self.device)))
 
     def __del__(self):
         if getattr(self, "ptr", None) and self.ptr.value:
