@@ -331,3 +331,39 @@ def test_plan_api_directly(ws, dev):
     torch.cuda.synchronize()
     lib.ws_gemm_plan_destroy(plan)
     assert np.array_equal(as_f64(c), _want(256, 256, 512))
+
+
+def test_repeat_call_fast_path_tracks_every_operand_property(ws, dev):
+    """gemm_tn's repeat-call path reuses a prepared launch only for the same addresses, shapes,
+    strides, dtypes and knobs: views over the same storage with a different shape or stride, a new
+    scale, and an out of another dtype each get their own validated plan (results stay exact), and
+    an invalid view at a cached address is still rejected."""
+    a = ref_tensor("a", (512, 1024), BF16, dev)
+    b = ref_tensor("b", (512, 1024), BF16, dev)
+    c = torch.empty(512, 512, dtype=F32, device=dev)
+    want = _want(512, 512, 1024)
+    for _ in range(2):  # the second call takes the fast path
+        ws.gemm_tn(a, b, c)
+        torch.cuda.synchronize()
+        assert np.array_equal(as_f64(c), want)
+    # same storage, half the rows (same data_ptr, other shape)
+    c2 = torch.empty(256, 512, dtype=F32, device=dev)
+    ws.gemm_tn(a[:256], b, c2)
+    torch.cuda.synchronize()
+    assert np.array_equal(as_f64(c2), want[:256])
+    # same pointers, other scale: the plan must not be reused
+    ws.gemm_tn(a, b, c, scale_a=0.5)
+    torch.cuda.synchronize()
+    assert np.array_equal(as_f64(c), want * 0.5)
+    ws.gemm_tn(a, b, c)
+    torch.cuda.synchronize()
+    assert np.array_equal(as_f64(c), want)
+    # out at the same address reinterpreted as bf16 (other dtype): tolerance of the 16-bit output
+    c16 = c.view(torch.bfloat16)[:, :512]
+    ws.gemm_tn(a, b, c16)
+    torch.cuda.synchronize()
+    assert rel_err(as_f64(c16), want) <= 1e-2
+    # same storage viewed with K-stride 2 (not row-major): still rejected after the cached calls
+    bad = a.as_strided((512, 512), (1024, 2))
+    with pytest.raises(ws.WsError):
+        ws.gemm_tn(bad, b[:, :512], c)
