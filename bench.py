@@ -914,20 +914,22 @@ def bench_e2e_kfront(ws, torch, dev, args, world, rank, max_over_ranks, barrier)
     rng = np.random.default_rng(2026)
     bufs = {"a": (rng.integers(-16, 17, (M, K)) / 4.0), "b": (rng.integers(-16, 17, (N, K)) / 4.0),
             "c": np.zeros((M, N))}
-    ws.run_kernel(text, bufs, pid_range=(lo, hi))  # warm: staging buffers, tensor maps
+    for _ in range(2):  # warm: staging buffers, tensor maps, the host pool; the first calls also
+        ws.run_kernel(text, bufs, pid_range=(lo, hi))  # run 2x slower while host pages settle
     barrier()
     reps = []
-    for _ in range(3):
+    for _ in range(5):
         t0 = time.perf_counter()
         ws.run_kernel(text, bufs, pid_range=(lo, hi))
         reps.append(time.perf_counter() - t0)
-    sec = max_over_ranks(sorted(reps)[1])
+    sec = max_over_ranks(sorted(reps)[2])
     n_loc = (hi - lo) // (M // 128) * 256
     return {"value": round(2.0 * M * N * K / sec / 1e12, 3), "unit": "TFLOP/s", "s_per_call": round(sec, 4),
             "h2d_bytes_per_step": (M * K + n_loc * K) * 2, "d2h_bytes_per_step": M * n_loc * 4,
             "path": "ws.run_kernel -> ws_run_kernel (the .k front end of ws::run): double host buffers in/out, "
-                    "bf16 staging converted on the host threads, fp32 result written back as double",
-            "workload": "gemm.k M=N=8192 K=2048 (128x256x64 .k tiles), median of 3 calls"}
+                    "bf16 staging converted on a host thread pool in row chunks overlapping the H2D; the fp32 "
+                    "result copied out in row chunks and written back as double while the next chunk is in flight",
+            "workload": "gemm.k M=N=8192 K=2048 (128x256x64 .k tiles), median of 5 calls after 2 warm-up calls"}
 
 
 def bench_e2e(ws, torch, dev, stream, args, world, max_over_ranks, barrier, n_range=(0, 8192)):

@@ -21,11 +21,16 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
+#include <condition_variable>
 #include <cstdint>
 #include <cstring>
+#include <exception>
+#include <functional>
 #include <map>
 #include <memory>
+#include <mutex>
 #include <set>
 #include <stdexcept>
 #include <string>
@@ -724,22 +729,92 @@ struct Staging {
 };
 thread_local Staging g_stage;
 
-// Host conversion loops over rows [0, n), split over host threads when large.
+// Host conversion loops over rows [0, n), split over a persistent pool of host threads when large
+// (spawning threads per loop cost ~0.3 ms a loop, and the pipelined GEMM path runs a loop per
+// row chunk). One loop runs at a time; the calling thread works too. An exception thrown by a row
+// (kfail) is rethrown in the caller.
+class RowPool {
+ public:
+  static RowPool& get() {
+    static RowPool* p = new RowPool();  // never destroyed: workers may still wait at process exit
+    return *p;
+  }
+  int threads() const { return static_cast<int>(th_.size()) + 1; }
+  void run(int64_t n, int64_t grain, const std::function<void(int64_t)>& f) {
+    std::lock_guard<std::mutex> job(job_mu_);
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      fn_ = &f;
+      n_ = n;
+      grain_ = std::max<int64_t>(1, grain);
+      next_.store(0);
+      err_ = nullptr;
+      active_ = static_cast<int>(th_.size());
+      ++gen_;
+    }
+    cv_.notify_all();
+    work();
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [&] { return active_ == 0; });
+    fn_ = nullptr;
+    if (err_) std::rethrow_exception(err_);
+  }
+
+ private:
+  RowPool() {
+    const int nt = static_cast<int>(std::min<unsigned>(std::max(1u, std::thread::hardware_concurrency()), 16u));
+    for (int t = 1; t < nt; ++t)
+      th_.emplace_back([this] {
+        uint64_t seen = 0;
+        for (;;) {
+          {
+            std::unique_lock<std::mutex> lk(mu_);
+            cv_.wait(lk, [&] { return gen_ != seen; });
+            seen = gen_;
+          }
+          work();
+          std::lock_guard<std::mutex> lk(mu_);
+          if (--active_ == 0) done_cv_.notify_all();
+        }
+      });
+    for (auto& t : th_) t.detach();
+  }
+  void work() {
+    for (;;) {
+      const int64_t i0 = next_.fetch_add(grain_);
+      if (i0 >= n_) return;
+      try {
+        for (int64_t i = i0; i < std::min(n_, i0 + grain_); ++i) (*fn_)(i);
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (!err_) err_ = std::current_exception();
+        next_.store(n_);
+      }
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex job_mu_, mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int64_t)>* fn_ = nullptr;
+  int64_t n_ = 0, grain_ = 1;
+  std::atomic<int64_t> next_{0};
+  std::exception_ptr err_;
+  int active_ = 0;
+  uint64_t gen_ = 0;
+};
+
 template <class F>
 void parallel_rows(int64_t n, int64_t work_per_row, F&& f) {
   const int64_t work = n * std::max<int64_t>(1, work_per_row);
-  int nt = static_cast<int>(std::min<int64_t>(std::thread::hardware_concurrency(), 16));
-  if (work < (int64_t(1) << 20) || nt <= 1 || n < 2) {
+  if (work < (int64_t(1) << 20) || n < 2) {
     for (int64_t i = 0; i < n; ++i) f(i);
     return;
   }
-  nt = static_cast<int>(std::min<int64_t>(nt, n));
-  std::vector<std::thread> th;
-  for (int t = 0; t < nt; ++t)
-    th.emplace_back([&, t] {
-      for (int64_t i = n * t / nt; i < n * (t + 1) / nt; ++i) f(i);
-    });
-  for (auto& x : th) x.join();
+  RowPool& pool = RowPool::get();
+  // ~4 grains per thread: balance without per-row atomics
+  const int64_t grain = std::max<int64_t>(1, n / (4 * pool.threads()));
+  const std::function<void(int64_t)> fn = [&](int64_t i) { f(i); };
+  pool.run(n, grain, fn);
 }
 
 const Op* def_of(const std::vector<Op>& ops, const std::string& v) {
@@ -1012,29 +1087,39 @@ bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo,
     const int64_t Mp = (M + 255) / 256 * 256, Np = (N + 255) / 256 * 256, Kp = (Kd + 63) / 64 * 64;
     auto* ha = static_cast<uint16_t*>(g_stage.pinned(0, static_cast<size_t>(Mp * Kp) * 2));
     auto* hb = static_cast<uint16_t*>(g_stage.pinned(1, static_cast<size_t>(Np * Kp) * 2));
-    parallel_rows(Mp, Kp, [&](int64_t r) {
-      uint16_t* row = ha + r * Kp;
-      if (r >= M) {
-        std::memset(row, 0, Kp * 2);
-        return;
-      }
-      for (int64_t k = 0; k < Kd; ++k) row[k] = to_half_bits(static_cast<float>(A.get(rmin + dA + r, ka0 + k)), dt);
-      for (int64_t k = Kd; k < Kp; ++k) row[k] = 0;
-    });
-    parallel_rows(Np, Kp, [&](int64_t n) {
-      uint16_t* row = hb + n * Kp;
-      if (n >= N) {
-        std::memset(row, 0, Kp * 2);
-        return;
-      }
-      for (int64_t k = 0; k < Kd; ++k) row[k] = to_half_bits(static_cast<float>(B.get(cmin + dB + n, kb0 + k)), dt);
-      for (int64_t k = Kd; k < Kp; ++k) row[k] = 0;
-    });
     void* da = g_stage.device(0, static_cast<size_t>(Mp * Kp) * 2);
     void* db = g_stage.device(1, static_cast<size_t>(Np * Kp) * 2);
     void* dc = g_stage.device(2, static_cast<size_t>(Mp * Np) * 4);
-    cuda_check(cudaMemcpyAsync(da, ha, static_cast<size_t>(Mp * Kp) * 2, cudaMemcpyHostToDevice, st), "H2D");
-    cuda_check(cudaMemcpyAsync(db, hb, static_cast<size_t>(Np * Kp) * 2, cudaMemcpyHostToDevice, st), "H2D");
+    // operands: converted to 16 bits and copied in row chunks, so the host->device copy of one
+    // chunk runs while the host threads convert the next
+    auto stage_in = [&](const HostBuf& X, int64_t rows, int64_t rows_p, int64_t r_src, int64_t k_src, uint16_t* h,
+                        void* d) {
+      const int64_t nch = rows_p >= 2048 ? 8 : 1;
+      const double* xr = X.shape.real ? static_cast<const double*>(X.data) : nullptr;
+      for (int64_t ch = 0; ch < nch; ++ch) {
+        const int64_t r0 = rows_p * ch / nch, r1 = rows_p * (ch + 1) / nch;
+        parallel_rows(r1 - r0, Kp, [&](int64_t i) {
+          const int64_t r = r0 + i;
+          uint16_t* row = h + r * Kp;
+          if (r >= rows) {
+            std::memset(row, 0, Kp * 2);
+            return;
+          }
+          if (xr) {
+            const double* src = xr + (r_src + r) * X.shape.c + k_src;
+            for (int64_t k = 0; k < Kd; ++k) row[k] = to_half_bits(static_cast<float>(src[k]), dt);
+          } else {
+            for (int64_t k = 0; k < Kd; ++k) row[k] = to_half_bits(static_cast<float>(X.get(r_src + r, k_src + k)), dt);
+          }
+          for (int64_t k = Kd; k < Kp; ++k) row[k] = 0;
+        });
+        cuda_check(cudaMemcpyAsync(static_cast<uint16_t*>(d) + r0 * Kp, h + r0 * Kp, static_cast<size_t>((r1 - r0) * Kp) * 2,
+                                   cudaMemcpyHostToDevice, st),
+                   "H2D");
+      }
+    };
+    stage_in(A, M, Mp, rmin + dA, ka0, ha, da);
+    stage_in(B, N, Np, cmin + dB, kb0, hb, db);
     ws_gemm_desc d{};
     d.in_dtype = dt;
     d.out_dtype = WS_F32;
@@ -1044,14 +1129,45 @@ bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo,
     gemm_launch_knobs(d, pl, Kp);
     d.act = act_relu ? 1 : 0;
     ws_check(ws_gemm_tn(&d, st));
+    // result: copied out in row chunks; the host threads write chunk i into the caller's buffer
+    // while chunk i+1 is in flight. Only the pids' own tiles are written (ref store_tile).
     auto* hc = static_cast<float*>(g_stage.pinned(2, static_cast<size_t>(Mp * Np) * 4));
-    cuda_check(cudaMemcpyAsync(hc, dc, static_cast<size_t>(Mp * Np) * 4, cudaMemcpyDeviceToHost, st), "D2H");
-    cuda_check(cudaStreamSynchronize(st), "sync");
-    parallel_rows(static_cast<int64_t>(ts.size()), BM * BN, [&](int64_t i) {
-      const PidTile& t = ts[static_cast<size_t>(i)];
-      for (int64_t r = 0; r < BM; ++r)
-        for (int64_t c = 0; c < BN; ++c) C.set(t.r0 + r, t.c0 + c, hc[(t.r0 - rmin + r) * Np + (t.c0 - cmin + c)]);
-    });
+    const int64_t nch = M >= 2048 ? 8 : 1;
+    std::vector<cudaEvent_t> evs(static_cast<size_t>(nch));
+    for (auto& e : evs) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    auto chunk_rows = [&](int64_t ch, int64_t& r0, int64_t& r1) {
+      r0 = M * ch / nch;
+      r1 = M * (ch + 1) / nch;
+    };
+    for (int64_t ch = 0; ch < nch; ++ch) {
+      int64_t r0, r1;
+      chunk_rows(ch, r0, r1);
+      cuda_check(cudaMemcpyAsync(hc + r0 * Np, static_cast<float*>(dc) + r0 * Np, static_cast<size_t>((r1 - r0) * Np) * 4,
+                                 cudaMemcpyDeviceToHost, st),
+                 "D2H");
+      cuda_check(cudaEventRecord(evs[static_cast<size_t>(ch)], st), "event");
+    }
+    double* cr = C.shape.real ? static_cast<double*>(C.data) : nullptr;
+    for (int64_t ch = 0; ch < nch; ++ch) {
+      int64_t r0, r1;  // rows relative to rmin
+      chunk_rows(ch, r0, r1);
+      cuda_check(cudaEventSynchronize(evs[static_cast<size_t>(ch)]), "sync");
+      parallel_rows(static_cast<int64_t>(ts.size()), BM * BN / nch, [&](int64_t i) {
+        const PidTile& t = ts[static_cast<size_t>(i)];
+        const int64_t lo_r = std::max(t.r0 - rmin, r0), hi_r = std::min(t.r0 - rmin + BM, r1);
+        for (int64_t rr = lo_r; rr < hi_r; ++rr) {
+          const float* src = hc + rr * Np + (t.c0 - cmin);
+          const int64_t r = rmin + rr;
+          if (cr) {
+            double* dst = cr + r * C.shape.c + t.c0;
+            for (int64_t c = 0; c < BN; ++c) dst[c] = src[c];
+          } else {
+            for (int64_t c = 0; c < BN; ++c) C.set(r, t.c0 + c, src[c]);
+          }
+        }
+      });
+    }
+    for (auto& e : evs) cudaEventDestroy(e);
   }
   return true;
 }
