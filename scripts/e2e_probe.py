@@ -53,3 +53,12 @@ print(f"D2H {d2h_bytes / 1e9:.2f} GB in {t_d:.2f} ms = {d2h_bytes / t_d / 1e6:.1
 print(f"both directions at once: {t_both:.2f} ms")
 print(f"gemm_tn_host step: {t_pipe:.2f} ms = {flops / t_pipe / 1e9:.1f} TFLOP/s "
       f"(H2D-only bound {flops / t_h / 1e9:.1f})")
+
+# job order: the sweep ascending in K front-loads 128 MB copy-outs behind tiny inputs and ends with
+# 512 MB inputs behind one copy-out; interleaving large and small K keeps both directions busy
+orders = {"ascending": list(range(len(KS))), "descending": list(range(len(KS)))[::-1],
+          "interleaved": [6, 0, 5, 1, 4, 2, 3], "interleaved_small_first": [0, 6, 1, 5, 2, 4, 3]}
+for name, order in orders.items():
+    js = [jobs[i] for i in order]
+    t = timed(lambda: ws.gemm_tn_host(js, device=dev))
+    print(f"order {name:24s} {[KS[i] for i in order]}: {t:.2f} ms = {flops / t / 1e9:.1f} TFLOP/s")
