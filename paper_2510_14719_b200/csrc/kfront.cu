@@ -37,6 +37,8 @@
 #include <thread>
 #include <vector>
 
+#include <unistd.h>
+
 #include "../../include/ws.h"
 
 namespace ws_detail {
@@ -736,7 +738,16 @@ thread_local Staging g_stage;
 class RowPool {
  public:
   static RowPool& get() {
-    static RowPool* p = new RowPool();  // never destroyed: workers may still wait at process exit
+    // never destroyed: workers may still wait at process exit. A forked child has none of the
+    // parent's worker threads, so it builds its own pool.
+    static std::mutex mu;
+    static RowPool* p = nullptr;
+    static pid_t owner = 0;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!p || owner != getpid()) {
+      p = new RowPool();
+      owner = getpid();
+    }
     return *p;
   }
   int threads() const { return static_cast<int>(th_.size()) + 1; }
