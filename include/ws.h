@@ -220,9 +220,11 @@ int32_t ws_watchdog(ws_watchdog_info* out);
 void ws_debug_gemm_trace(unsigned long long* trace);
 
 /* Developer diagnostics: subsequent ws_gemm_tn launches have CTA 0 store {%clock64, %globaltimer}
- * at its start and when it retires into `clk` (a device buffer of 4 uint64; the last launch's
- * stamps win), so the SM clock a launch ran at is (clk[2]-clk[0]) / (clk[3]-clk[1]) GHz — the
- * per-clock efficiency of a measured kernel without an external sampler. NULL turns it off. */
+ * at its start and when it retires into `clk` (a zeroed device buffer of 8 uint64; the last
+ * launch's stamps win), so the SM clock a launch ran at is (clk[2]-clk[0]) / (clk[3]-clk[1]) GHz,
+ * and add the two spans and 1 to running totals clk[4], clk[5], clk[6] (the mean clock over every
+ * probed launch is clk[4] / clk[5] GHz) — the per-clock efficiency of a measured kernel without an
+ * external sampler. NULL turns it off. */
 void ws_debug_gemm_clock(unsigned long long* clk);
 
 #ifdef __cplusplus

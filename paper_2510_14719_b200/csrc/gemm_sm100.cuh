@@ -50,7 +50,8 @@ struct GemmParams {
   int debug_deadlock;  // WS_DEBUG_DEADLOCK: CTA 0 skips its first put (watchdog demonstration)
   int batch;           // independent products stacked along rows (gemm_batched.k); >= 1
   // clock probe (ws_debug_gemm_clock): CTA 0 stores {%clock64, %globaltimer} when it starts and
-  // when it retires, so the SM clock during this launch is dclock / dns; nullptr = off
+  // when it retires, so the SM clock during this launch is dclock / dns, and adds both spans and a
+  // launch count to running totals (clk[4..6]); nullptr = off
   unsigned long long* clk;
 };
 
@@ -489,8 +490,13 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
     tmem_dealloc<CG>(tmem_base, TMEM_COLS);
   }
   if (p.clk && blockIdx.x == 0 && threadIdx.x == 64) {
-    p.clk[2] = clock64();
-    p.clk[3] = globaltimer();
+    const unsigned long long c1 = clock64(), g1 = globaltimer();
+    p.clk[2] = c1;
+    p.clk[3] = g1;
+    // running totals over every probed launch: the mean clock of a set of launches
+    p.clk[4] += c1 - p.clk[0];
+    p.clk[5] += g1 - p.clk[1];
+    p.clk[6] += 1;
   }
 #undef GT
 }
