@@ -89,6 +89,10 @@ def _gemm_desc(ws, **kw):
     (dict(bn=96), "type"),
     (dict(lda=128), "type"),
     (dict(act=2), "type"),
+    (dict(M=0), "type"),                            # empty products are refused, not launched
+    (dict(N=0), "type"),
+    (dict(K=0), "type"),
+    (dict(M=-256), "type"),
 ])
 def test_gemm_validation_codes(ws, kw, code):
     lib = ws._lib.load()
@@ -134,6 +138,9 @@ def _attn_desc(ws, **kw):
     (dict(dtype=3, kv_block=64), "unsupported-kernel"),
     (dict(dtype=3, D=5), "smem-overflow"),          # FP8: f16 P and V buffers leave room for 4 K slots
     (dict(bh_begin=1, bh_end=1), "type"),
+    (dict(S=0), "type"),                            # empty inputs are refused, not launched
+    (dict(B=0), "type"),
+    (dict(H=0), "type"),
 ])
 def test_attn_validation_codes(ws, kw, code):
     lib = ws._lib.load()
