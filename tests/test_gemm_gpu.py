@@ -367,3 +367,34 @@ def test_repeat_call_fast_path_tracks_every_operand_property(ws, dev):
     bad = a.as_strided((512, 512), (1024, 2))
     with pytest.raises(ws.WsError):
         ws.gemm_tn(bad, b[:, :512], c)
+
+
+def test_clock_probe_sums_every_probed_launch(ws, dev):
+    """ws_debug_gemm_clock: CTA 0's %clock64 / %globaltimer spans are summed over every probed
+    launch (clk[4], clk[5]) with a launch count (clk[6]); the mean clock they give is a plausible
+    SM clock, and launches after the probe is turned off leave the buffer alone."""
+    import ctypes
+
+    lib = ws._lib.load()
+    a = ref_tensor("a", (1024, 2048), BF16, dev)
+    b = ref_tensor("b", (1024, 2048), BF16, dev)
+    c = torch.empty(1024, 1024, dtype=F32, device=dev)
+    clk = torch.zeros(8, dtype=torch.int64, device=dev)
+    ws.gemm_tn(a, b, c)  # plan built before probing
+    torch.cuda.synchronize()
+    lib.ws_debug_gemm_clock(ctypes.c_void_p(clk.data_ptr()))
+    try:
+        for _ in range(3):
+            ws.gemm_tn(a, b, c)
+        torch.cuda.synchronize()
+    finally:
+        lib.ws_debug_gemm_clock(None)
+    v = clk.cpu().tolist()
+    assert v[6] == 3
+    assert v[2] > v[0] and v[3] > v[1]
+    ghz = v[4] / v[5]
+    assert 0.3 < ghz < 2.5, ghz
+    ws.gemm_tn(a, b, c)
+    torch.cuda.synchronize()
+    assert clk.cpu().tolist() == v
+    assert np.array_equal(as_f64(c), _want(1024, 1024, 2048))
