@@ -530,6 +530,7 @@ __global__ void __launch_bounds__(A128_THREADS, 1)
       // P_t's shared-memory tile is free once PV_t(j-1) has read it (long done by now: PV_t(j-1) was
       // issued when this warp finished block j-1)
       if (g + j > 0) mbar_wait(a_pvdone, (g + j - 1) & 1, 24 + t);
+      if (tr) WS_TRACE(1 + t, g + j, 6);
       if (j == 0 && it > 0) {
         // the previous item's O_t was staged through this P tile: its TMA store must have read it
         if (warp == 4u * t && lane == 0) tma_store_wait_read<0>();
