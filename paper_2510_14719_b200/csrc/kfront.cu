@@ -1144,7 +1144,14 @@ bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo,
     // while chunk i+1 is in flight. Only the pids' own tiles are written (ref store_tile).
     auto* hc = static_cast<float*>(g_stage.pinned(2, static_cast<size_t>(Mp * Np) * 4));
     const int64_t nch = M >= 2048 ? 8 : 1;
-    std::vector<cudaEvent_t> evs(static_cast<size_t>(nch));
+    struct Events {  // destroyed on every exit, kfail included
+      std::vector<cudaEvent_t> v;
+      ~Events() {
+        for (cudaEvent_t e : v) cudaEventDestroy(e);
+      }
+    } ev;
+    ev.v.assign(static_cast<size_t>(nch), nullptr);
+    std::vector<cudaEvent_t>& evs = ev.v;
     for (auto& e : evs) cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
     auto chunk_rows = [&](int64_t ch, int64_t& r0, int64_t& r1) {
       r0 = M * ch / nch;
@@ -1178,7 +1185,6 @@ bool try_gemm(const Kernel& g, std::map<std::string, HostBuf>& bufs, int64_t lo,
         }
       });
     }
-    for (auto& e : evs) cudaEventDestroy(e);
   }
   return true;
 }
