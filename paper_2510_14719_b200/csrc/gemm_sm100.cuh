@@ -405,8 +405,8 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
         }
       };
       if constexpr (EARLY_RELEASE) {
-        // half h: wait for its MMAs, load this warp's 32 rows x 128 columns (16 at a time, the next
-        // load in flight during each conversion), release the TMEM half, then stage and store. The
+        // half h: wait for its MMAs, load this warp's 32 rows x 128 columns (all loads in flight at
+        // once), release the TMEM half, then convert, stage and store. The
         // MMA warp's next tile waits for the TMEM reads only (scripts/gemm_trace.py: with the
         // release after the stores the tensor core idled ~5500 cycles per tile at K = 2048).
         constexpr int HC = MMA_N / 2;  // columns per warp per half
@@ -416,23 +416,16 @@ __global__ void __launch_bounds__(GEMM_THREADS, 1)
           tc_fence_after();
           if (tw && hc == 0) GT(ti, 6 + 3 * h);
           const uint32_t t_row = tmem_base + ((q * 32u) << 16) + h * MMA_N + hc * HC;
-          uint32_t pk[HC / 2];
-          uint32_t va[16], vb[16];
-          tmem_ld16(t_row, va);
+          // all HC columns in flight at once and one wait: the TMEM half goes back to the MMA warp
+          // after a single load latency, and the conversion runs after the release
+          uint32_t raw[HC];
 #pragma unroll
-          for (int i = 0; i < HC / 16; ++i) {
-            tmem_wait_ld();
-            if (i + 1 < HC / 16) {
-              if (i & 1)
-                tmem_ld16(t_row + (i + 1) * 16, va);
-              else
-                tmem_ld16(t_row + (i + 1) * 16, vb);
-            }
-            const uint32_t* cur = (i & 1) ? vb : va;
-#pragma unroll
-            for (int j = 0; j < 8; ++j) pk[i * 8 + j] = cvt2(cur[2 * j], cur[2 * j + 1]);
-          }
+          for (int i = 0; i < HC / 32; ++i) tmem_ld32(t_row + i * 32, *reinterpret_cast<uint32_t(*)[32]>(&raw[i * 32]));
+          tmem_wait_ld();
           release_acc(h, 7 + 3 * h);
+          uint32_t pk[HC / 2];
+#pragma unroll
+          for (int j = 0; j < HC / 2; ++j) pk[j] = cvt2(raw[2 * j], raw[2 * j + 1]);
 #pragma unroll
           for (int ch = 0; ch < HC / CW; ++ch) stage_store(pk + ch * 32, nb * BN + h * MMA_N + hc * HC + ch * CW);
           if (tw && hc == 0) GT(ti, 8 + 3 * h);
