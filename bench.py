@@ -41,10 +41,10 @@ K_SWEEP = [256, 512, 1024, 2048, 4096, 8192, 16384]
 METRIC = "GEMM & attention-fwd TFLOPS at 1/2/4/8 B200, % of tensor-core peak"
 WORKLOAD = ("C2: bf16 GEMM c = a.b^T, M=N=8192 (global; N-column sharded over the GPUs), "
             "K sweep 256..16384, one pass = 7 launches")
-TILE_POLICY = ("library auto policy: cta_group::2 CTA pairs (M % 256 == 0, K >= 256); < 16 K blocks (K < 1024): "
-               "256x256x64 pair tiles (D=6, raster group 2, TMEM double-buffered); >= 16 K blocks: 256x512x64 "
-               "pair tiles (D=4, group 16, one TMEM accumulator handed over N half by N half, early-release "
-               "epilogue)")
+TILE_POLICY = ("library auto policy: cta_group::2 CTA pairs (M % 256 == 0, K >= 256); 256x512x64 pair tiles "
+               "from 4 K blocks on, i.e. at every K of the sweep (D=4, raster group 16, one TMEM accumulator handed "
+               "over N half by N half, early-release epilogue); 256x256 pairs below 4 K blocks or where 512-wide "
+               "tiles would not fill the GPU")
 
 
 def gemm_flops(K, M=M_, N=N_):
@@ -497,7 +497,7 @@ def run_ours(args):
     peak = peaks["bf16"] if burst else peaks["bf16_sustained"]
     roofline = {"bound": "tensor", "achieved": round(achieved, 1), "peak": peak,
                 "unit": "TFLOP/s", "frac": round(achieved / peak, 4), "traffic": traffic,
-                "kernel": f"ws_gemm_tn_kernel<bf16,bf16,{512 if Kd >= 1024 else 256},cta_group::2> M=8192 N={n_loc} K={Kd}",
+                "kernel": f"ws_gemm_tn_kernel<bf16,bf16,{512 if n_loc % 512 == 0 else 256},cta_group::2> M=8192 N={n_loc} K={Kd}",
                 "peak_kind": (f"bf16_tflops {'burst' if burst else 'sustained'} ({peaks['source']}): the timed "
                               f"region is {region_ms:.0f} ms"),
                 "frac_of_burst": round(achieved / peaks["bf16"], 4),

@@ -714,8 +714,11 @@ ws_status build_plan(const ws_gemm_desc* desc, ws_gemm_plan& pl) {
   // (256 x 256 pairs are L2 -> SM bandwidth bound, ~600 instead of 512 cycles per K block); its
   // single TMEM accumulator is handed over half by half with an early-release epilogue
   const int64_t kblocks = d.K / (128 / (eb > 0 ? eb : 1));
-  // auto: 256 x 512 pair tiles from 16 K blocks on (bf16 K >= 1024, FP8 K >= 2048; 4-7% over
-  // 256 x 256 pairs there, equal at 8 K blocks; scripts/gemm_policy_sweep.sh), else 256-wide
+  // auto: 256 x 512 pair tiles from 4 K blocks on (4-7% over 256 x 256 pairs from 16 K blocks,
+  // scripts/gemm_policy_sweep.sh; and, since the epilogue releases each accumulator half after one
+  // batched TMEM load, 2-5% at 4-12 K blocks too: bf16 K = 256 / 512 / 768 and FP8
+  // K = 512 / 1024 / 1536, profiles/r02n_ab_gemm_short_k_tiles.txt; FP8 K = 256, 2 K blocks, was
+  // 5% slower), else 256-wide
   // ... and only when the grid still fills the GPU: small problems take the smaller tile with
   // more work units (1024^3: 128 x 128 single-CTA tiles, 64 CTAs)
   const int64_t units = num_sms();
@@ -732,7 +735,7 @@ ws_status build_plan(const ws_gemm_desc* desc, ws_gemm_plan& pl) {
   const bool fill256 = nbat * (d.M / 128) * (d.N / 256) >= units;
   // (N a multiple of 128 but not of 256: 128-wide tiles, single CTA or pair)
   int bn = d.bn > 0 ? d.bn
-           : (d.cta_pair && kblocks >= 16 && d.N % 512 == 0 && fill512) ? 512
+           : (d.cta_pair && kblocks >= 4 && d.N % 512 == 0 && fill512)   ? 512
            : (!d.cta_pair && !fill256 && d.N % 128 == 0)                 ? 128
            : (d.N % 256 != 0 && d.N % 128 == 0)                          ? 128
                                                                          : 256;
