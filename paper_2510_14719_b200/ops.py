@@ -73,7 +73,7 @@ def gemm_tn(a: torch.Tensor, b: torch.Tensor, out: Optional[torch.Tensor] = None
     out: optional [M,N] tensor (may be a column slice of a wider matrix; its row stride is ldc).
     cta_pair: None = auto (cta_group::2 CTA pairs when M % 256 == 0, K >= 256 and the pair tiles
     fill the GPU; single-CTA tiles otherwise).
-    bn: 0 = auto (the library picks 256 x 512 pair tiles from 16 K blocks when they fill the GPU,
+    bn: 0 = auto (the library picks 256 x 512 pair tiles from 4 K blocks when they fill the GPU,
     else 256-wide tiles, or 128-wide single-CTA tiles for small problems).
     """
     if out is not None:
